@@ -1,0 +1,401 @@
+"""``B200Backend``: the reference ``Backend`` contract on libpfgpu.so.
+
+Drop-in for ``ToolchainBackend`` (`/root/reference/pkg/src/phaseforge/
+backend/toolchain.py:276-307`) behind the ABC of `backend/types.py:121-152`:
+
+* ``compile(kernel, order)``: the order is interpreted by ``passmodel`` into
+  a transformation state, which selects one precompiled sm_100a variant; the
+  artifact is that variant's SASS (normalised), so identical machine code
+  yields identical digests.  Pure in (kernel, order).
+* ``execute(..., VALIDATION)``: one untimed run on the small stock input,
+  outputs read back (never timed, explorer.py:203).
+* ``execute(..., MEASUREMENT)``: a CUDA-event-timed run on the measurement
+  input (never validated, explorer.py:210-211); wall time in seconds.
+* ``execute(..., random_input_index=n)``: the n-th random validation-size
+  input, generated on the device (the ``<validation_input>#n`` descriptor of
+  toolchain.py:231-233).
+* ``measurement_lock``: one lock per backend, and one backend per device.
+
+Error mapping: a CUDA failure returns ``CRASH`` and resets the
+device; a run slower than ``set_timeout_override`` returns ``TIMEOUT``
+(toolchain.py:250-258 kills the runner; an in-process kernel cannot be
+killed, so every variant is bounded by construction); configuration errors
+raise ``BackendError``.  There is no CPU path: without libpfgpu.so this module
+does not import.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import gzip
+import json
+import statistics
+from collections import OrderedDict
+from ctypes import byref, c_double, c_float, c_int, c_int64, c_void_p
+from pathlib import Path
+
+from .. import _abi, passmodel, registry
+from ..catalog import PhaseOrder
+from .types import (
+    Artifact,
+    Backend,
+    BackendError,
+    CompileOutcome,
+    ExecutionOutcome,
+    ExecutionStatus,
+    InputKind,
+    KernelCase,
+)
+
+ARTIFACTS_PATH = Path(__file__).resolve().parent.parent / "artifacts.json.gz"
+ARTIFACT_MAGIC = "pfgpu-artifact/1"
+
+
+class Workspace:
+    """One benchmark instance resident on one GPU (owns a ``pf_ws``)."""
+
+    def __init__(self, device: int, bench: str, dims: tuple[int, ...]):
+        self.lib = _abi.lib()
+        self.device = device
+        self.bench = bench
+        self.bench_id = registry.bench_index(bench)
+        self.dims = tuple(int(d) for d in dims)
+        self._dims_c = _abi.dims_array(self.dims)
+        handle = c_void_p()
+        _abi.check(self.lib.pf_ws_create(device, self.bench_id, self._dims_c, byref(handle)))
+        self.handle = handle
+        info = bench_arrays(bench)
+        self.arrays = info
+        self.elems = []
+        for a in range(len(info)):
+            n = c_int64()
+            _abi.check(self.lib.pf_array_elems(self.bench_id, self._dims_c, a, byref(n)))
+            self.elems.append(n.value)
+        self.nbytes = 4 * sum(self.elems) + 4 * sum(
+            n for (_, role, _), n in zip(info, self.elems) if role == _abi.ROLE_INOUT
+        )
+        self.input_tag = None
+        self.warm: set[int] = set()
+
+    def generate(self, stock: bool, seed: int, instance: int) -> None:
+        tag = (bool(stock), int(seed), int(instance))
+        if self.input_tag == tag:
+            return
+        _abi.check(self.lib.pf_ws_generate(self.handle, int(stock), seed, instance))
+        self.input_tag = tag
+
+    def run(self, variant: int, samples: int = 1, batch: int = 1, restore: bool = True,
+            flush: bool = False) -> list[float]:
+        ms = (c_float * samples)()
+        _abi.check(self.lib.pf_run(self.handle, variant, samples, batch, int(restore), int(flush), ms))
+        return list(ms)
+
+    def run_e2e(self, variant: int, samples: int, host_in, host_out) -> list[float]:
+        ms = (c_float * samples)()
+        n = len(self.arrays)
+        hin = (c_void_p * n)(*[host_in.get(a) for a in range(n)])
+        hout = (c_void_p * n)(*[host_out.get(a) for a in range(n)])
+        _abi.check(self.lib.pf_run_e2e(self.handle, variant, samples, hin, hout, ms))
+        return list(ms)
+
+    def download(self, array: int):
+        import numpy as np
+
+        out = np.empty(self.elems[array], dtype=np.float32)
+        _abi.check(self.lib.pf_ws_download(self.handle, array, out.ctypes.data_as(c_void_p), out.size))
+        return out
+
+    def upload(self, array: int, data) -> None:
+        import numpy as np
+
+        buf = np.ascontiguousarray(data, dtype=np.float32).ravel()
+        _abi.check(self.lib.pf_ws_upload(self.handle, array, buf.ctypes.data_as(c_void_p), buf.size))
+        self.input_tag = None
+
+    def outputs(self) -> list:
+        return [self.download(a) for a, (_, _, is_out) in enumerate(self.arrays) if is_out]
+
+    def checksum(self, array: int) -> tuple[float, float]:
+        s, a = c_double(), c_double()
+        _abi.check(self.lib.pf_checksum(self.handle, array, byref(s), byref(a)))
+        return s.value, a.value
+
+    def compare(self, ref: "Workspace", rtol: float, atol_rel: float) -> tuple[float, int]:
+        err, bad = c_double(), c_int64()
+        _abi.check(self.lib.pf_compare(self.handle, ref.handle, rtol, atol_rel, byref(err), byref(bad)))
+        return err.value, bad.value
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.pf_ws_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_ARRAY_CACHE: dict[str, list[tuple[str, int, int]]] = {}
+
+
+def bench_arrays(bench: str) -> list[tuple[str, int, int]]:
+    """[(name, role, is_output)] of a benchmark's arrays, from the library."""
+    if bench not in _ARRAY_CACHE:
+        lib = _abi.lib()
+        bid = registry.bench_index(bench)
+        narr = c_int()
+        _abi.check(lib.pf_bench_info(bid, None, 0, None, byref(narr)))
+        rows = []
+        for a in range(narr.value):
+            name = ctypes.create_string_buffer(64)
+            role, out = c_int(), c_int()
+            _abi.check(lib.pf_array_info(bid, a, name, 64, byref(role), byref(out)))
+            rows.append((name.value.decode(), role.value, out.value))
+        _ARRAY_CACHE[bench] = rows
+    return _ARRAY_CACHE[bench]
+
+
+_FAMILIES: dict[str, passmodel.VariantFamily] = {}
+
+
+def family(bench: str) -> passmodel.VariantFamily:
+    if bench not in _FAMILIES:
+        lib = _abi.lib()
+        bid = registry.bench_index(bench)
+        n = lib.pf_variant_count(bid)
+        if n <= 0:
+            raise BackendError(f"benchmark {bench!r} is not built into libpfgpu.so")
+        knobs = []
+        buf = (c_int * _abi.NKNOBS)()
+        for v in range(n):
+            _abi.check(lib.pf_variant_knobs(bid, v, buf))
+            knobs.append(tuple(buf))
+        _FAMILIES[bench] = passmodel.VariantFamily(bench, knobs)
+    return _FAMILIES[bench]
+
+
+_ARTIFACT_TEXT: dict | None = None
+
+
+def _artifact_table() -> dict:
+    global _ARTIFACT_TEXT
+    if _ARTIFACT_TEXT is None:
+        if not ARTIFACTS_PATH.exists():
+            raise BackendError(f"{ARTIFACTS_PATH.name} missing: run tools/gen_artifacts.py (part of build())")
+        _ARTIFACT_TEXT = json.loads(gzip.decompress(ARTIFACTS_PATH.read_bytes()))["benches"]
+    return _ARTIFACT_TEXT
+
+
+def variant_sass(bench: str, variant: int) -> str:
+    try:
+        return _artifact_table()[bench][str(variant)]
+    except KeyError as exc:
+        raise BackendError(f"no SASS recorded for {bench} variant {variant}") from exc
+
+
+def variant_launches(bench: str, variant: int, dims) -> int:
+    n = c_int64()
+    _abi.check(_abi.lib().pf_variant_launches(registry.bench_index(bench), variant, _abi.dims_array(dims), byref(n)))
+    return n.value
+
+
+def alg_work(bench: str, dims) -> tuple[float, float]:
+    b, f = c_double(), c_double()
+    _abi.check(_abi.lib().pf_alg_work(registry.bench_index(bench), _abi.dims_array(dims), byref(b), byref(f)))
+    return b.value, f.value
+
+
+def device_count() -> int:
+    n = c_int()
+    rc = _abi.lib().pf_device_count(byref(n))
+    return n.value if rc == 0 else 0
+
+
+class B200Backend(Backend):
+    """compile = variant lookup; execute = device-timed run (see module doc)."""
+
+    def __init__(
+        self,
+        device: int = 0,
+        samples: int = 5,
+        seed: int = 1729,
+        flush_l2: bool = True,
+        min_sample_ms: float = 0.05,
+        max_batch: int = 64,
+        memory_budget: float = 100e9,
+    ):
+        super().__init__()
+        self.lib = _abi.lib()
+        self.device = device
+        self.samples = samples
+        self.seed = seed
+        self.flush_l2 = flush_l2
+        self.min_sample_ms = min_sample_ms
+        self.max_batch = max_batch
+        self.memory_budget = memory_budget
+        self._ws: "OrderedDict[tuple, Workspace]" = OrderedDict()
+        self._artifacts: dict[tuple[str, int], Artifact] = {}
+        self._batch: dict[tuple, int] = {}
+        self._timeouts: dict[str, float] = {}
+        self.device_runs = 0
+        self.kernel_launches = 0
+
+    # ------------------------------------------------------------ helpers
+    def set_timeout_override(self, kernel_id: str, timeout: float) -> None:
+        """Runs slower than ``timeout`` seconds report TIMEOUT (cli.py:194-195)."""
+        if timeout <= 0:
+            raise ValueError(f"timeout must be positive, got {timeout}")
+        self._timeouts[kernel_id] = timeout
+
+    def variant_for(self, kernel: KernelCase, order: PhaseOrder) -> tuple[str, int]:
+        bench = registry.bench_of(kernel)
+        return bench, family(bench).select(passmodel.interpret(order))
+
+    def artifact(self, bench: str, variant: int) -> Artifact:
+        key = (bench, variant)
+        art = self._artifacts.get(key)
+        if art is None:
+            knobs = family(bench).knobs[variant]
+            header = f"{ARTIFACT_MAGIC} bench={bench} launch=stage{knobs[0]}\n"
+            art = Artifact.from_content((header + variant_sass(bench, variant)).encode())
+            self._artifacts[key] = art
+        return art
+
+    def workspace(self, bench: str, dims: tuple[int, ...], stock: bool, instance: int) -> Workspace:
+        key = (bench, tuple(dims), "stock" if stock else "random")
+        ws = self._ws.get(key)
+        if ws is None:
+            ws = Workspace(self.device, bench, dims)
+            self._ws[key] = ws
+            self._evict(keep=key)
+        else:
+            self._ws.move_to_end(key)
+        ws.generate(stock, self.seed, instance)
+        return ws
+
+    def _evict(self, keep) -> None:
+        total = sum(w.nbytes for w in self._ws.values())
+        for key in list(self._ws):
+            if total <= self.memory_budget:
+                break
+            if key == keep:
+                continue
+            w = self._ws.pop(key)
+            total -= w.nbytes
+            w.close()
+
+    def close(self) -> None:
+        for w in self._ws.values():
+            w.close()
+        self._ws.clear()
+
+    def _crash(self, exc: _abi.PfError) -> ExecutionOutcome:
+        # A sticky CUDA error poisons the context: drop every workspace and reset.
+        for w in self._ws.values():
+            w.handle = None  # memory dies with the context
+        self._ws.clear()
+        self.lib.pf_device_reset(self.device)
+        return ExecutionOutcome(ExecutionStatus.CRASH, log=str(exc))
+
+    def _supported(self, bench: str, variant: int, dims) -> bool:
+        rc = self.lib.pf_variant_supported(registry.bench_index(bench), variant, _abi.dims_array(dims))
+        return rc == 0
+
+    # ------------------------------------------------------------ Backend API
+    def compile(self, kernel: KernelCase, order: PhaseOrder) -> CompileOutcome:
+        bench, variant = self.variant_for(kernel, order)
+        for text in (kernel.validation_input, kernel.measurement_input):
+            _, dims = registry.parse_descriptor(text)
+            if not self._supported(bench, variant, dims):
+                return CompileOutcome.codegen_failure(
+                    f"{bench} variant {family(bench).key(variant)} does not support {text}"
+                )
+        return CompileOutcome.success(self.artifact(bench, variant))
+
+    def execute(
+        self,
+        kernel: KernelCase,
+        order: PhaseOrder,
+        artifact: Artifact,
+        input_kind: InputKind,
+        random_input_index: int | None = None,
+    ) -> ExecutionOutcome:
+        bench, variant = self.variant_for(kernel, order)
+        if self.artifact(bench, variant).digest != artifact.digest:
+            raise BackendError(f"artifact {artifact.digest[:12]} was not compiled from this order for {kernel.id!r}")
+        try:
+            if random_input_index is not None or input_kind is InputKind.VALIDATION:
+                _, dims = registry.parse_descriptor(kernel.validation_input)
+                stock = random_input_index is None
+                ws = self.workspace(bench, dims, stock, -1 if stock else int(random_input_index))
+                ms = ws.run(variant, samples=1, batch=1, restore=True, flush=False)
+                self._count(bench, variant, dims, 1)
+                outs = ws.outputs()
+                values = tuple(float(x) for arr in outs for x in arr.tolist())
+                return self._finish(kernel, ms[0], values)
+            _, dims = registry.parse_descriptor(kernel.measurement_input)
+            ws = self.workspace(bench, dims, True, -1)
+            ms = self._timed(ws, variant)
+            return self._finish(kernel, statistics.median(ms), None)
+        except _abi.PfError as exc:
+            if exc.code == _abi.PF_ECUDA:
+                return self._crash(exc)
+            raise BackendError(str(exc)) from exc
+
+    def _finish(self, kernel: KernelCase, ms: float, outputs) -> ExecutionOutcome:
+        seconds = max(ms, 1e-6) * 1e-3
+        limit = self._timeouts.get(kernel.id)
+        if limit is not None and seconds > limit:
+            return ExecutionOutcome(ExecutionStatus.TIMEOUT, log=f"{seconds:.6f}s > timeout {limit:.6f}s")
+        return ExecutionOutcome(ExecutionStatus.VALID, wall_time=seconds, outputs=outputs)
+
+    def _count(self, bench: str, variant: int, dims, runs: int) -> None:
+        self.device_runs += runs
+        self.kernel_launches += runs * variant_launches(bench, variant, dims)
+
+    def _timed(self, ws: Workspace, variant: int) -> list[float]:
+        """Median-of-``samples`` device time of one run (ms).  The first use of
+        a (workspace, variant) does an untimed warm-up and sizes the batch so a
+        sample spans at least ``min_sample_ms`` (us-scale kernels)."""
+        key = (ws.bench, ws.dims, variant)
+        if variant not in ws.warm:
+            first = ws.run(variant, samples=1, batch=1, restore=True, flush=False)[0]
+            self._count(ws.bench, variant, ws.dims, 1)
+            ws.warm.add(variant)
+            if key not in self._batch:
+                batch = 1
+                if first < self.min_sample_ms:
+                    batch = min(self.max_batch, max(1, int(self.min_sample_ms / max(first, 1e-4)) + 1))
+                self._batch[key] = batch
+        batch = self._batch.get(key, 1)
+        ms = ws.run(variant, samples=self.samples, batch=batch, restore=True, flush=self.flush_l2)
+        self._count(ws.bench, variant, ws.dims, self.samples * batch)
+        return ms
+
+    # ------------------------------------------------------------ conveniences
+    def baseline_outputs(self, kernel: KernelCase) -> tuple[float, ...]:
+        """Validation-input outputs of the empty-order (baseline) variant."""
+        compiled = self.compile(kernel, PhaseOrder())
+        if not compiled.is_ok:
+            raise BackendError(f"baseline compile failed for {kernel.id!r}")
+        out = self.execute(kernel, PhaseOrder(), compiled.artifact, InputKind.VALIDATION)
+        if out.status is not ExecutionStatus.VALID or out.outputs is None:
+            raise BackendError(f"baseline validation run failed for {kernel.id!r}: {out.log}")
+        return out.outputs
+
+    def time_variant(self, bench: str, dims, variant: int, samples: int | None = None) -> float:
+        """Median device time (s) of ``variant`` on the stock input at ``dims``."""
+        ws = self.workspace(bench, tuple(dims), True, -1)
+        old = self.samples
+        if samples:
+            self.samples = samples
+        try:
+            return statistics.median(self._timed(ws, variant)) * 1e-3
+        finally:
+            self.samples = old
+
+
+__all__ = ["B200Backend", "Workspace", "alg_work", "bench_arrays", "device_count", "family", "variant_launches",
+           "variant_sass"]

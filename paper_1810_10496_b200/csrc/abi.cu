@@ -1,0 +1,573 @@
+// C-ABI implementation of libpfgpu.so (see include/pfgpu.h).
+//
+// Replaces the subprocess runner of the reference's ToolchainBackend
+// (/root/reference/pkg/src/phaseforge/backend/toolchain.py:216-273): inputs
+// are generated on the device, a run is timed with CUDA events on the
+// workspace's own stream, and outputs are copied back on request.
+#include "pf_common.cuh"
+#include "../../include/pfgpu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+struct pf_ws : pf::Workspace {};
+
+namespace pf {
+
+namespace {
+
+thread_local std::string g_err;
+
+const BenchDesc** registry() {
+  static const BenchDesc* table[B_COUNT] = {};
+  return table;
+}
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return PF_ECUDA;
+}
+
+#define PF_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+// Per-device L2 flush buffer (2 x L2), grown lazily under a lock.
+struct FlushBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_flush_mu;
+FlushBuf g_flush[64];
+
+int flush_l2(int device, cudaStream_t s) {
+  FlushBuf* fb;
+  {
+    std::lock_guard<std::mutex> lk(g_flush_mu);
+    fb = &g_flush[device];
+    if (!fb->ptr) {
+      int l2 = 0;
+      PF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+      size_t want = std::max<size_t>((size_t)l2 * 2, (size_t)64 << 20);
+      PF_CUDA(cudaMalloc(&fb->ptr, want));
+      fb->bytes = want;
+    }
+  }
+  PF_CUDA(cudaMemsetAsync(fb->ptr, 0x5a, fb->bytes, s));
+  return PF_OK;
+}
+
+const BenchDesc* bench_desc(int bench) {
+  if (bench < 0 || bench >= B_COUNT) return nullptr;
+  return registry()[bench];
+}
+
+int check_bench(int bench, const BenchDesc** d) {
+  if (bench < 0 || bench >= B_COUNT) return fail(PF_EINVAL, "bench index out of range");
+  *d = registry()[bench];
+  if (!*d) return fail(PF_ENOTBUILT, "benchmark module not compiled into libpfgpu");
+  return PF_OK;
+}
+
+Dims to_dims(const BenchDesc* d, const int64_t* dims) {
+  Dims out{};
+  for (int i = 0; i < kMaxDims; ++i) out.d[i] = (i < d->ndims) ? dims[i] : 0;
+  return out;
+}
+
+int set_device(int device) {
+  PF_CUDA(cudaSetDevice(device));
+  return PF_OK;
+}
+
+// ---- device-side comparison --------------------------------------------------
+__global__ void absmax_kernel(const float* __restrict__ r, int64_t n, unsigned int* out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(r[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // non-negative floats order as uints
+}
+
+__global__ void compare_kernel(const float* __restrict__ t, const float* __restrict__ r, int64_t n,
+                               double rtol, const unsigned int* absmax_bits, double atol_rel,
+                               unsigned long long* nbad, unsigned int* maxerr_bits) {
+  double atol = atol_rel * (double)__uint_as_float(*absmax_bits);
+  float worst = 0.f;
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double rv = r[i], tv = t[i];
+    double diff = fabs(tv - rv);
+    double tol = fmax(atol, rtol * fabs(rv));
+    bool ok = diff <= tol;  // NaN fails
+    if (!ok) ++bad;
+    double denom = fmax(fabs(rv), atol);
+    double e = ok ? (denom > 0 ? diff / denom : 0.0) : (denom > 0 && diff == diff ? diff / denom : 3.0e38);
+    worst = fmaxf(worst, (float)fmin(e, 3.0e38));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    worst = fmaxf(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(maxerr_bits, __float_as_uint(worst));
+    if (bad) atomicAdd(nbad, bad);
+  }
+}
+
+__global__ void checksum_kernel(const float* __restrict__ x, int64_t n, double* out) {
+  double s = 0, a = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    s += x[i];
+    a += fabs((double)x[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], s);
+    atomicAdd(&out[1], a);
+  }
+}
+
+struct GraphCache {
+  std::unordered_map<int, cudaGraphExec_t> exec;
+};
+
+}  // namespace
+
+void register_bench(int id, const BenchDesc* desc) {
+  if (id >= 0 && id < B_COUNT) registry()[id] = desc;
+}
+
+float* Workspace::ensure_scratch(size_t bytes) {
+  if (scratch_bytes >= bytes) return scratch;
+  if (scratch) cudaFree(scratch);
+  scratch = nullptr;
+  scratch_bytes = 0;
+  if (cudaMalloc(&scratch, bytes) != cudaSuccess) return nullptr;
+  scratch_bytes = bytes;
+  return scratch;
+}
+
+// Graph-staged variants capture their launch sequence once per workspace.
+cudaGraphExec_t cached_graph(Workspace& ws, int key, void (*body)(Workspace&, cudaStream_t)) {
+  auto* gc = static_cast<GraphCache*>(ws.graphs);
+  if (!gc) {
+    gc = new GraphCache();
+    ws.graphs = gc;
+  }
+  auto it = gc->exec.find(key);
+  if (it != gc->exec.end()) return it->second;
+  cudaStream_t cap;
+  cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+  cudaGraph_t g;
+  cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+  body(ws, cap);
+  cudaStreamEndCapture(cap, &g);
+  cudaGraphExec_t ex = nullptr;
+  cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cap);
+  gc->exec[key] = ex;
+  return ex;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_abi_version(void) { return PFGPU_ABI_VERSION; }
+
+const char* pf_last_error(void) { return g_err.c_str(); }
+
+int pf_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *count = n;
+  return PF_OK;
+}
+
+int pf_device_reset(int device) {
+  {
+    std::lock_guard<std::mutex> lk(g_flush_mu);
+    g_flush[device] = FlushBuf{};  // memory dies with the context
+  }
+  int rc = set_device(device);
+  if (rc) return rc;
+  PF_CUDA(cudaDeviceReset());
+  return PF_OK;
+}
+
+int pf_device_info(int device, char* name, size_t len, int* sm_count, int64_t* l2_bytes, int* cc_major,
+                   int* cc_minor) {
+  cudaDeviceProp p;
+  PF_CUDA(cudaGetDeviceProperties(&p, device));
+  if (name && len) {
+    std::snprintf(name, len, "%s", p.name);
+  }
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (l2_bytes) *l2_bytes = p.l2CacheSize;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return PF_OK;
+}
+
+int pf_bench_count(void) { return B_COUNT; }
+
+int pf_bench_info(int bench, char* name, size_t len, int* ndims, int* narrays) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  if (name && len) std::snprintf(name, len, "%s", d->name);
+  if (ndims) *ndims = d->ndims;
+  if (narrays) *narrays = d->narrays;
+  return PF_OK;
+}
+
+int pf_bench_dim_name(int bench, int dim, char* name, size_t len) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  if (dim < 0 || dim >= d->ndims) return fail(PF_EINVAL, "dim index out of range");
+  std::snprintf(name, len, "%s", d->dim_names[dim]);
+  return PF_OK;
+}
+
+int pf_array_info(int bench, int array, char* name, size_t len, int* role, int* is_output) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  if (array < 0 || array >= d->narrays) return fail(PF_EINVAL, "array index out of range");
+  if (name && len) std::snprintf(name, len, "%s", d->arrays[array].name);
+  if (role) *role = d->arrays[array].role;
+  if (is_output) *is_output = d->arrays[array].is_output;
+  return PF_OK;
+}
+
+int pf_array_elems(int bench, const int64_t* dims, int array, int64_t* elems) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  if (array < 0 || array >= d->narrays) return fail(PF_EINVAL, "array index out of range");
+  *elems = d->array_elems(array, to_dims(d, dims));
+  return PF_OK;
+}
+
+int pf_alg_work(int bench, const int64_t* dims, double* bytes, double* flops) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  Dims dd = to_dims(d, dims);
+  if (bytes) *bytes = d->alg_bytes(dd);
+  if (flops) *flops = d->alg_flops(dd);
+  return PF_OK;
+}
+
+int pf_variant_count(int bench) {
+  const BenchDesc* d = bench_desc(bench);
+  return d ? d->nvariants : 0;
+}
+
+int pf_variant_knobs(int bench, int variant, int* knobs) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  if (variant < 0 || variant >= d->nvariants) return fail(PF_EINVAL, "variant index out of range");
+  const Knobs& k = d->variants[variant];
+  knobs[0] = k.stage;
+  knobs[1] = k.store;
+  knobs[2] = k.unroll;
+  knobs[3] = k.lsr;
+  knobs[4] = k.vec;
+  return PF_OK;
+}
+
+int pf_variant_launches(int bench, int variant, const int64_t* dims, int64_t* launches) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  if (variant < 0 || variant >= d->nvariants) return fail(PF_EINVAL, "variant index out of range");
+  *launches = d->launches(variant, to_dims(d, dims));
+  return PF_OK;
+}
+
+int pf_variant_supported(int bench, int variant, const int64_t* dims) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  if (variant < 0 || variant >= d->nvariants) return fail(PF_EINVAL, "variant index out of range");
+  if (d->check && d->check(variant, to_dims(d, dims)) != 0)
+    return fail(PF_EINVAL, "variant does not support these dims");
+  return PF_OK;
+}
+
+int pf_ws_create(int device, int bench, const int64_t* dims, pf_ws** out) {
+  const BenchDesc* d;
+  if (int rc = check_bench(bench, &d)) return rc;
+  for (int i = 0; i < d->ndims; ++i)
+    if (dims[i] < 1) return fail(PF_EINVAL, "dims must be positive");
+  if (int rc = set_device(device)) return rc;
+  auto* ws = new pf_ws();
+  std::memset(static_cast<Workspace*>(ws), 0, sizeof(Workspace));
+  ws->device = device;
+  ws->bench = bench;
+  ws->desc = d;
+  ws->dims = to_dims(d, dims);
+  for (int a = 0; a < d->narrays; ++a) {
+    int64_t n = d->array_elems(a, ws->dims);
+    ws->elems[a] = n;
+    size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(float);
+    if (cudaMalloc(&ws->a.p[a], bytes) != cudaSuccess) {
+      pf_ws_destroy(ws);
+      return fail(PF_ENOMEM, "cudaMalloc failed for array " + std::string(d->arrays[a].name));
+    }
+    if (d->arrays[a].role == INOUT) {
+      if (cudaMalloc(&ws->pristine[a], bytes) != cudaSuccess) {
+        pf_ws_destroy(ws);
+        return fail(PF_ENOMEM, "cudaMalloc failed for pristine copy");
+      }
+    }
+  }
+  PF_CUDA(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking));
+  PF_CUDA(cudaEventCreate(&ws->ev0));
+  PF_CUDA(cudaEventCreate(&ws->ev1));
+  *out = ws;
+  return PF_OK;
+}
+
+int pf_ws_destroy(pf_ws* ws) {
+  if (!ws) return PF_OK;
+  cudaSetDevice(ws->device);
+  if (ws->stream) cudaStreamSynchronize(ws->stream);
+  for (int a = 0; a < kMaxArrays; ++a) {
+    if (ws->a.p[a]) cudaFree(ws->a.p[a]);
+    if (ws->pristine[a]) cudaFree(ws->pristine[a]);
+  }
+  if (ws->scratch) cudaFree(ws->scratch);
+  if (ws->graphs) {
+    auto* gc = static_cast<GraphCache*>(ws->graphs);
+    for (auto& kv : gc->exec) cudaGraphExecDestroy(kv.second);
+    delete gc;
+  }
+  if (ws->ev0) cudaEventDestroy(ws->ev0);
+  if (ws->ev1) cudaEventDestroy(ws->ev1);
+  if (ws->stream) cudaStreamDestroy(ws->stream);
+  delete ws;
+  return PF_OK;
+}
+
+static int snapshot(pf_ws* ws) {
+  const BenchDesc* d = ws->desc;
+  for (int a = 0; a < d->narrays; ++a)
+    if (d->arrays[a].role == INOUT)
+      PF_CUDA(cudaMemcpyAsync(ws->pristine[a], ws->a.p[a], ws->elems[a] * sizeof(float),
+                              cudaMemcpyDeviceToDevice, ws->stream));
+  return PF_OK;
+}
+
+int pf_ws_generate(pf_ws* ws, int stock, uint64_t seed, int64_t instance) {
+  if (int rc = set_device(ws->device)) return rc;
+  const BenchDesc* d = ws->desc;
+  for (int a = 0; a < d->narrays; ++a) {
+    if (d->arrays[a].role == OUT) {
+      PF_CUDA(cudaMemsetAsync(ws->a.p[a], 0, ws->elems[a] * sizeof(float), ws->stream));
+    } else {
+      d->launch_init(ws->a.p[a], a, ws->elems[a], ws->dims, stock, seed, instance, ws->stream);
+    }
+  }
+  PF_CUDA(cudaGetLastError());
+  if (int rc = snapshot(ws)) return rc;
+  PF_CUDA(cudaStreamSynchronize(ws->stream));
+  return PF_OK;
+}
+
+int pf_ws_upload(pf_ws* ws, int array, const float* host, int64_t n) {
+  if (array < 0 || array >= ws->desc->narrays) return fail(PF_EINVAL, "array index out of range");
+  if (n != ws->elems[array]) return fail(PF_EINVAL, "element count mismatch");
+  if (int rc = set_device(ws->device)) return rc;
+  PF_CUDA(cudaMemcpyAsync(ws->a.p[array], host, n * sizeof(float), cudaMemcpyHostToDevice, ws->stream));
+  if (ws->pristine[array])
+    PF_CUDA(cudaMemcpyAsync(ws->pristine[array], ws->a.p[array], n * sizeof(float), cudaMemcpyDeviceToDevice,
+                            ws->stream));
+  PF_CUDA(cudaStreamSynchronize(ws->stream));
+  return PF_OK;
+}
+
+int pf_ws_download(pf_ws* ws, int array, float* host, int64_t n) {
+  if (array < 0 || array >= ws->desc->narrays) return fail(PF_EINVAL, "array index out of range");
+  if (n != ws->elems[array]) return fail(PF_EINVAL, "element count mismatch");
+  if (int rc = set_device(ws->device)) return rc;
+  PF_CUDA(cudaMemcpyAsync(host, ws->a.p[array], n * sizeof(float), cudaMemcpyDeviceToHost, ws->stream));
+  PF_CUDA(cudaStreamSynchronize(ws->stream));
+  return PF_OK;
+}
+
+static int restore_async(pf_ws* ws) {
+  const BenchDesc* d = ws->desc;
+  for (int a = 0; a < d->narrays; ++a) {
+    if (d->arrays[a].role == INOUT)
+      PF_CUDA(cudaMemcpyAsync(ws->a.p[a], ws->pristine[a], ws->elems[a] * sizeof(float),
+                              cudaMemcpyDeviceToDevice, ws->stream));
+    else if (d->arrays[a].role == OUT)
+      PF_CUDA(cudaMemsetAsync(ws->a.p[a], 0, ws->elems[a] * sizeof(float), ws->stream));
+  }
+  return PF_OK;
+}
+
+int pf_ws_restore(pf_ws* ws) {
+  if (int rc = set_device(ws->device)) return rc;
+  if (int rc = restore_async(ws)) return rc;
+  PF_CUDA(cudaStreamSynchronize(ws->stream));
+  return PF_OK;
+}
+
+int pf_ws_array_ptr(pf_ws* ws, int array, void** dptr) {
+  if (array < 0 || array >= ws->desc->narrays) return fail(PF_EINVAL, "array index out of range");
+  *dptr = ws->a.p[array];
+  return PF_OK;
+}
+
+int pf_run(pf_ws* ws, int variant, int samples, int batch, int restore, int flush, float* ms) {
+  const BenchDesc* d = ws->desc;
+  if (variant < 0 || variant >= d->nvariants) return fail(PF_EINVAL, "variant index out of range");
+  if (samples < 1 || batch < 1) return fail(PF_EINVAL, "samples and batch must be >= 1");
+  if (d->check && d->check(variant, ws->dims) != 0) return fail(PF_EINVAL, "variant does not support these dims");
+  if (int rc = set_device(ws->device)) return rc;
+  RunFn fn = d->run[variant];
+  for (int s = 0; s < samples; ++s) {
+    if (restore)
+      if (int rc = restore_async(ws)) return rc;
+    if (flush)
+      if (int rc = flush_l2(ws->device, ws->stream)) return rc;
+    PF_CUDA(cudaEventRecord(ws->ev0, ws->stream));
+    for (int b = 0; b < batch; ++b) fn(*ws, ws->stream);
+    PF_CUDA(cudaGetLastError());
+    PF_CUDA(cudaEventRecord(ws->ev1, ws->stream));
+    PF_CUDA(cudaEventSynchronize(ws->ev1));
+    float t = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&t, ws->ev0, ws->ev1));
+    ms[s] = t / (float)batch;
+  }
+  return PF_OK;
+}
+
+int pf_run_e2e(pf_ws* ws, int variant, int samples, float* const* host_in, float* const* host_out, float* ms) {
+  const BenchDesc* d = ws->desc;
+  if (variant < 0 || variant >= d->nvariants) return fail(PF_EINVAL, "variant index out of range");
+  if (d->check && d->check(variant, ws->dims) != 0) return fail(PF_EINVAL, "variant does not support these dims");
+  if (int rc = set_device(ws->device)) return rc;
+  RunFn fn = d->run[variant];
+  for (int s = 0; s < samples; ++s) {
+    PF_CUDA(cudaEventRecord(ws->ev0, ws->stream));
+    for (int a = 0; a < d->narrays; ++a) {
+      size_t bytes = ws->elems[a] * sizeof(float);
+      if (d->arrays[a].role == OUT) {
+        PF_CUDA(cudaMemsetAsync(ws->a.p[a], 0, bytes, ws->stream));
+      } else if (host_in && host_in[a]) {
+        PF_CUDA(cudaMemcpyAsync(ws->a.p[a], host_in[a], bytes, cudaMemcpyHostToDevice, ws->stream));
+      }
+    }
+    fn(*ws, ws->stream);
+    PF_CUDA(cudaGetLastError());
+    for (int a = 0; a < d->narrays; ++a)
+      if (d->arrays[a].is_output && host_out && host_out[a])
+        PF_CUDA(cudaMemcpyAsync(host_out[a], ws->a.p[a], ws->elems[a] * sizeof(float), cudaMemcpyDeviceToHost,
+                                ws->stream));
+    PF_CUDA(cudaEventRecord(ws->ev1, ws->stream));
+    PF_CUDA(cudaEventSynchronize(ws->ev1));
+    float t = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&t, ws->ev0, ws->ev1));
+    ms[s] = t;
+  }
+  return PF_OK;
+}
+
+int pf_compare(pf_ws* test, pf_ws* ref, double rtol, double atol_rel, double* max_err, int64_t* nbad) {
+  if (test->bench != ref->bench) return fail(PF_EINVAL, "workspaces hold different benchmarks");
+  for (int i = 0; i < kMaxDims; ++i)
+    if (test->dims.d[i] != ref->dims.d[i]) return fail(PF_EINVAL, "workspaces have different dims");
+  if (test->device != ref->device) return fail(PF_EINVAL, "workspaces live on different devices");
+  if (int rc = set_device(test->device)) return rc;
+  cudaStreamSynchronize(ref->stream);
+  unsigned int* dev = nullptr;  // [absmax, maxerr] + nbad(u64)
+  PF_CUDA(cudaMalloc(&dev, 16));
+  double worst = 0.0;
+  long long bad_total = 0;
+  const BenchDesc* d = test->desc;
+  for (int a = 0; a < d->narrays; ++a) {
+    if (!d->arrays[a].is_output) continue;
+    int64_t n = test->elems[a];
+    cudaMemsetAsync(dev, 0, 16, test->stream);
+    unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    if (blocks < 1) blocks = 1;
+    absmax_kernel<<<blocks, 256, 0, test->stream>>>(ref->a.p[a], n, dev);
+    compare_kernel<<<blocks, 256, 0, test->stream>>>(test->a.p[a], ref->a.p[a], n, rtol, dev, atol_rel,
+                                                     reinterpret_cast<unsigned long long*>(dev + 2), dev + 1);
+    unsigned int h[4];
+    cudaError_t e = cudaMemcpyAsync(h, dev, 16, cudaMemcpyDeviceToHost, test->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(test->stream);
+    if (e != cudaSuccess) {
+      cudaFree(dev);
+      return cuda_fail(e, "pf_compare");
+    }
+    float me;
+    std::memcpy(&me, &h[1], 4);
+    unsigned long long nb;
+    std::memcpy(&nb, &h[2], 8);
+    worst = std::max(worst, (double)me);
+    bad_total += (long long)nb;
+  }
+  cudaFree(dev);
+  *max_err = worst;
+  *nbad = bad_total;
+  return PF_OK;
+}
+
+int pf_checksum(pf_ws* ws, int array, double* sum, double* abs_sum) {
+  if (array < 0 || array >= ws->desc->narrays) return fail(PF_EINVAL, "array index out of range");
+  if (int rc = set_device(ws->device)) return rc;
+  double* dev = nullptr;
+  PF_CUDA(cudaMalloc(&dev, 16));
+  cudaMemsetAsync(dev, 0, 16, ws->stream);
+  int64_t n = ws->elems[array];
+  unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+  checksum_kernel<<<blocks, 256, 0, ws->stream>>>(ws->a.p[array], n, dev);
+  double h[2];
+  cudaError_t e = cudaMemcpyAsync(h, dev, 16, cudaMemcpyDeviceToHost, ws->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
+  cudaFree(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "pf_checksum");
+  *sum = h[0];
+  *abs_sum = h[1];
+  return PF_OK;
+}
+
+int pf_host_alloc(size_t bytes, void** ptr) {
+  PF_CUDA(cudaMallocHost(ptr, bytes));
+  return PF_OK;
+}
+
+int pf_host_free(void* ptr) {
+  PF_CUDA(cudaFreeHost(ptr));
+  return PF_OK;
+}
+
+}  // extern "C"

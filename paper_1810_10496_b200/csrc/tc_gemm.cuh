@@ -1,0 +1,342 @@
+// Stage-2 contraction kernel: tcgen05 / TMEM 3xTF32 GEMM for sm_100a.
+//
+//   D = alpha * op(A) op(B) + beta * Cin          (fp32 in, fp32 out)
+//   op(A)(m,k) = ta ? A[k*lda + m] : A[m*lda + k]
+//   op(B)(k,n) = tb ? B[n*ldb + k] : B[k*ldb + n]
+//   optional K-concatenated second product: + op(A2) op(B2)  (SYR2K)
+//
+// 3xTF32: x = hi + lo with hi = rna_tf32(x), lo = rna_tf32(x - hi); the
+// product is accumulated as lo*hi + hi*lo + hi*hi in the fp32 TMEM
+// accumulator (the lo*lo term, ~2^-22 relative, is dropped).  This keeps the
+// fp32 tolerance (1e-4 relative, BASELINE.json north_star) on tensor cores.
+//
+// Data path:
+//   1. tc_pack: reads op(A)/op(B) in either major-ness, splits, and writes the
+//      hi/lo operands as ready-made 128x32 K-major SWIZZLE_128B shared-memory
+//      images (16 KB each), one per (row block, k block).
+//   2. tc_gemm_kernel (128 threads, 1 CTA/SM, 128x128 output tile):
+//        warp0.lane0  producer: 4 x cp.async.bulk (16 KB) per k block into a
+//                     3-stage ring, completion via mbarrier complete_tx
+//        warp1.lane0  MMA issuer: 4 k-steps x 3 tcgen05.mma.kind::tf32
+//                     (M=128, N=128, K=8) per k block; tcgen05.commit frees
+//                     the stage; a final commit signals the epilogue
+//        warp2        TMEM allocator (128 columns)
+//        warps0-3     epilogue: tcgen05.ld 32x32b.x32 -> alpha/beta -> global
+#pragma once
+#include "pf_common.cuh"
+
+namespace pf {
+
+struct TcGemmArgs {
+  int M, N, K;
+  float alpha, beta;
+  const float* A;
+  int lda;
+  bool ta;
+  const float* B;
+  int ldb;
+  bool tb;
+  const float* A2;  // optional: K-concatenated second operand pair
+  const float* B2;
+  const float* Cin;  // may alias D; unused if beta == 0
+  int ldc;
+  float* D;
+  int ldd;
+  int upper_only;  // compute only output tiles with n-block >= m-block
+};
+
+constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
+constexpr uint32_t kTcTile = 16384;  // 128 rows x 32 fp32
+constexpr uint32_t kTcSmem = kTcStages * 4 * kTcTile + 1024;
+
+struct TcParams {
+  const float* ahi;
+  const float* alo;
+  const float* bhi;
+  const float* blo;
+  int kblocks;
+  int M, N;
+  float alpha, beta;
+  const float* Cin;
+  int ldc;
+  float* D;
+  int ldd;
+  int upper_only;
+};
+
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, SWIZZLE_128B UMMA shared-memory descriptor (sm100 layout):
+// start>>4 @[0,14), LBO>>4 @[16,30) (unused for swizzled K-major), SBO>>4
+// @[32,46) = 1024 B between 8-row groups, version 1 @[46,48), layout 2 @[61,64).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32 (bit 4), A/B tf32 (2 @7, 2 @10),
+// K-major A and B, N>>3 @[17,23), M>>4 @[24,29).
+constexpr uint32_t idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+}  // namespace tc
+
+// Pack op(X) (R x K logical, rows = M for A / N for B) into hi/lo K-major
+// SW128 tile images.  value(r,k) = kmajor ? X[r*ld + k] : X[k*ld + r];
+// k >= K reads X2 at k-K (K-concatenation).  Zero padding to 128 x 32.
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) tc_pack(const float* __restrict__ X, const float* __restrict__ X2, int ld,
+                                               int kmajor, int R, int K, int ktot, int kblocks,
+                                               float* __restrict__ hi, float* __restrict__ lo) {
+  const int kb = blockIdx.x, rb = blockIdx.y;
+  float* thi = hi + ((size_t)rb * kblocks + kb) * (kTcTile / 4);
+  float* tlo = lo + ((size_t)rb * kblocks + kb) * (kTcTile / 4);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = threadIdx.x + 256 * i;  // 16-byte chunk id in the tile
+    int r, c;
+    if (kmajor) {
+      r = q >> 3;
+      c = q & 7;
+    } else {
+      r = q & 127;
+      c = q >> 7;
+    }
+    const int gr = rb * kTcBM + r;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int k = kb * kTcBK + c * 4 + e;
+      float x = 0.f;
+      if (gr < R && k < ktot) {
+        const float* src = X;
+        if (k >= K) {
+          src = X2;
+          k -= K;
+        }
+        x = kmajor ? src[(size_t)gr * ld + k] : src[(size_t)k * ld + gr];
+      }
+      v[e] = x;
+    }
+    float4 h, l;
+    h.x = tc::tf32_rna(v[0]);
+    h.y = tc::tf32_rna(v[1]);
+    h.z = tc::tf32_rna(v[2]);
+    h.w = tc::tf32_rna(v[3]);
+    l.x = tc::tf32_rna(v[0] - h.x);
+    l.y = tc::tf32_rna(v[1] - h.y);
+    l.z = tc::tf32_rna(v[2] - h.z);
+    l.w = tc::tf32_rna(v[3] - h.w);
+    const int off = (r >> 3) * 256 + (r & 7) * 32 + ((c ^ (r & 7)) << 2);  // in floats
+    *reinterpret_cast<float4*>(thi + off) = h;
+    *reinterpret_cast<float4*>(tlo + off) = l;
+  }
+}
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], accum_bar;
+  __shared__ uint32_t tmem_slot;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mb = blockIdx.y, nb = blockIdx.x;
+  if (p.upper_only && nb < mb) return;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      tc::mbar_init(tc::smem_u32(&full_bar[s]), 1);
+      tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
+    }
+    tc::mbar_init(tc::smem_u32(&accum_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_slot)),
+                 "r"(128u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  const size_t a_base = (size_t)mb * p.kblocks * (kTcTile / 4);
+  const size_t b_base = (size_t)nb * p.kblocks * (kTcTile / 4);
+
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < p.kblocks; ++kb) {
+      const int s = kb % kTcStages;
+      const uint32_t ph = (kb / kTcStages) & 1;
+      tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
+      const uint32_t fb = tc::smem_u32(&full_bar[s]);
+      tc::mbar_expect_tx(fb, 4 * kTcTile);
+      const uint32_t dst = tc::smem_u32(smem + (size_t)s * 4 * kTcTile);
+      const size_t ko = (size_t)kb * (kTcTile / 4);
+      tc::bulk_g2s(dst, p.ahi + a_base + ko, kTcTile, fb);
+      tc::bulk_g2s(dst + kTcTile, p.alo + a_base + ko, kTcTile, fb);
+      tc::bulk_g2s(dst + 2 * kTcTile, p.bhi + b_base + ko, kTcTile, fb);
+      tc::bulk_g2s(dst + 3 * kTcTile, p.blo + b_base + ko, kTcTile, fb);
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, kTcBN);
+    for (int kb = 0; kb < p.kblocks; ++kb) {
+      const int s = kb % kTcStages;
+      const uint32_t ph = (kb / kTcStages) & 1;
+      tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
+      tc::fence_after();
+      const uint32_t base = tc::smem_u32(smem + (size_t)s * 4 * kTcTile);
+#pragma unroll
+      for (int kk = 0; kk < kTcBK / 8; ++kk) {
+        const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+        const uint64_t ahi = tc::desc_sw128(base + koff);
+        const uint64_t alo = tc::desc_sw128(base + kTcTile + koff);
+        const uint64_t bhi = tc::desc_sw128(base + 2 * kTcTile + koff);
+        const uint64_t blo = tc::desc_sw128(base + 3 * kTcTile + koff);
+        tc::mma_tf32(tmem, alo, bhi, idesc, (kb | kk) != 0);
+        tc::mma_tf32(tmem, ahi, blo, idesc, 1u);
+        tc::mma_tf32(tmem, ahi, bhi, idesc, 1u);
+      }
+      tc::mma_commit(tc::smem_u32(&empty_bar[s]));
+    }
+    tc::mma_commit(tc::smem_u32(&accum_bar));
+  }
+  __syncwarp();
+
+  // Epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31.
+  tc::mbar_wait(tc::smem_u32(&accum_bar), 0);
+  tc::fence_after();
+  const int row = mb * kTcBM + warp * 32 + lane;
+#pragma unroll 1
+  for (int c = 0; c < kTcBN / 32; ++c) {
+    uint32_t r[32];
+    tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32), r);
+    const int col0 = nb * kTcBN + c * 32;
+    if (row < p.M) {
+      float* drow = p.D + (size_t)row * p.ldd;
+      const float* crow = p.Cin + (size_t)row * p.ldc;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = col0 + j;
+        if (col < p.N) {
+          float v = p.alpha * __uint_as_float(r[j]);
+          if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
+          drow[col] = v;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u));
+  }
+}
+
+inline int64_t tc_gemm_launches(bool /*dual*/) { return 3; }  // pack A, pack B, gemm
+inline bool tc_gemm_supported(int64_t m, int64_t n, int64_t k) { return m > 0 && n > 0 && k > 0; }
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+template <BenchId Bn, int V>
+inline void launch_tc_gemm(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
+  const int ktot = a.A2 ? 2 * a.K : a.K;
+  const int mp = round_up(a.M, kTcBM), np = round_up(a.N, kTcBN), kp = round_up(ktot, kTcBK);
+  const int kblocks = kp / kTcBK;
+  const size_t asz = (size_t)mp * kp, bsz = (size_t)np * kp;
+  float* scr = ws.ensure_scratch((2 * asz + 2 * bsz) * sizeof(float));
+  if (!scr) return;  // allocation failure surfaces as a missing launch -> output mismatch
+  float* ahi = scr;
+  float* alo = ahi + asz;
+  float* bhi = alo + asz;
+  float* blo = bhi + bsz;
+  tc_pack<Bn, V><<<dim3(kblocks, mp / kTcBM), 256, 0, s>>>(a.A, a.A2, a.lda, a.ta ? 0 : 1, a.M, a.K, ktot, kblocks,
+                                                            ahi, alo);
+  tc_pack<Bn, V><<<dim3(kblocks, np / kTcBN), 256, 0, s>>>(a.B, a.B2, a.ldb, a.tb ? 1 : 0, a.N, a.K, ktot, kblocks,
+                                                            bhi, blo);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tc_gemm_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+    configured = true;
+  }
+  TcParams p{ahi, alo, bhi, blo, kblocks, a.M, a.N, a.alpha, a.beta, a.Cin, a.ldc, a.D, a.ldd, a.upper_only};
+  tc_gemm_kernel<Bn, V><<<dim3(np / kTcBN, mp / kTcBM), 128, kTcSmem, s>>>(p);
+}
+
+}  // namespace pf

@@ -1,0 +1,187 @@
+"""Phase order -> kernel variant: the deterministic pass-semantics interpreter.
+
+The reference compiles an order with clang/opt/llvm-link/codegen
+(`/root/reference/pkg/src/phaseforge/backend/toolchain.py:122-175`); none of
+that toolchain exists for sm_100a, so ``compile`` here interprets the order
+into the transformation state the paper attributes to phase orders in PTX
+ and selects the precompiled sm_100a variant that
+implements exactly that state.  This is a documented design decision, not
+reference behaviour.  It is pure in the order, so digests are
+stable, and it is order-sensitive (Fig. 5).
+
+Interpretation, left to right over the order (empty order = the baseline,
+i.e. the nvcc/PolyBench code shape):
+
+* alias analysis (``cfl-anders-aa``, ``cfl-steens-aa``, ``basicaa``,
+  ``scoped-noalias``, ``tbaa``, ``globals-aa``) is an immutable analysis in
+  LLVM's legacy pass manager, so its presence anywhere in the order counts;
+* ``licm`` with alias analysis available promotes the loop-carried store to a
+  register accumulator (store promotion -- the paper's main effect for 2MM,
+  3MM, GEMM, ATAX, BICG, MVT, SYRK, SYR2K, GRAMSCHM, CORR, COVAR);
+* ``reg2mem`` demotes values to stack slots; a later ``mem2reg``/``sroa``
+  re-promotes them.  A promoted accumulator left demoted is the
+  ``__local_depot`` shape of CORR/COVAR;
+* ``loop-reduce`` strength-reduces address arithmetic;
+* each ``loop-unroll`` doubles the unroll factor of the reduction loop
+  (1, 2, 4, then 8); without it an LLVM-compiled loop stays rolled;
+* a vectoriser (``bb-vectorize``, ``slp-vectorizer``,
+  ``load-store-vectorizer``, ``loop-vectorize``) running after the loop was
+  unrolled at least x4 forms 128-bit loads;
+* Blackwell staging: ``loop-interchange`` (needs alias analysis and a
+  promoted accumulator) re-maps the loop nest onto warps / smem tiles
+  (stage 1); a later ``loop-data-prefetch`` adds the asynchronous staging
+  stage (stage 2: fused single-pass, TMA/bulk-copy pipelines, tcgen05
+  tiles, CUDA-graph sequences).
+* every other pass (``print-memdeps``, ``dse``, ``gvn``, ...) leaves the
+  selected variant unchanged, so distinct orders share artifacts -- the
+  digest reuse of PAPER.md:163.
+
+Table-1 orders map to store-promoted variants for every
+kernel except GESUMMV (no ``licm``), which the unit tests pin.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .catalog import PassCatalog, PhaseOrder
+
+ALIAS_ANALYSES = frozenset({"cfl-anders-aa", "cfl-steens-aa", "basicaa", "scoped-noalias", "tbaa", "globals-aa"})
+VECTORIZERS = frozenset({"bb-vectorize", "slp-vectorizer", "load-store-vectorizer", "loop-vectorize"})
+REPROMOTERS = frozenset({"mem2reg", "sroa"})
+
+STORE_RMW, STORE_REG, STORE_DEPOT = 0, 1, 2
+STORE_NAMES = ("rmw", "reg", "depot")
+KNOB_NAMES = ("stage", "store", "unroll", "lsr", "vec")
+
+# The 20 Table-1 passes ...
+TABLE1_PASSES = (
+    "cfl-anders-aa", "dse", "loop-reduce", "licm", "instcombine", "gvn-hoist", "reg2mem", "sroa",
+    "bb-vectorize", "gvn", "sink", "loop-extract-single", "loop-unswitch", "ipsccp",
+    "nvptx-lower-alloca", "reassociate", "jump-threading", "print-memdeps", "mem2reg", "loop-unroll",
+)
+# ... plus LLVM 3.9 passes that expose the Blackwell staging choices.
+STAGING_PASSES = ("slp-vectorizer", "load-store-vectorizer", "loop-interchange", "loop-data-prefetch")
+
+DEFAULT_CATALOG_PASSES = TABLE1_PASSES + STAGING_PASSES
+
+
+def default_catalog() -> PassCatalog:
+    return PassCatalog.of(*DEFAULT_CATALOG_PASSES)
+
+
+@dataclass(frozen=True)
+class VariantState:
+    """Generic transformation state; ``unroll == 0`` only for the empty order."""
+
+    stage: int
+    store: int
+    unroll: int
+    lsr: int
+    vec: int
+
+    def as_tuple(self) -> tuple[int, int, int, int, int]:
+        return (self.stage, self.store, self.unroll, self.lsr, self.vec)
+
+    def key(self) -> str:
+        return (
+            f"stage={self.stage},store={STORE_NAMES[self.store]},unroll={self.unroll},"
+            f"lsr={self.lsr},vec={self.vec}"
+        )
+
+
+BASELINE_STATE = VariantState(stage=0, store=STORE_RMW, unroll=0, lsr=0, vec=0)
+
+
+def interpret(order: PhaseOrder) -> VariantState:
+    """The transformation state a phase order produces (see module docstring)."""
+    names = [p.name for p in order.passes]
+    if not names:
+        return BASELINE_STATE
+    have_aa = any(n in ALIAS_ANALYSES for n in names)
+    promoted = demoted = lsr = vec = interchanged = prefetched = False
+    unrolls = 0
+    for n in names:
+        if n == "licm":
+            promoted = promoted or have_aa
+        elif n == "reg2mem":
+            demoted = True
+        elif n in REPROMOTERS:
+            demoted = False
+        elif n == "loop-reduce":
+            lsr = True
+        elif n == "loop-unroll":
+            unrolls += 1
+        elif n in VECTORIZERS:
+            vec = vec or unrolls >= 2
+        elif n == "loop-interchange":
+            interchanged = interchanged or have_aa
+        elif n == "loop-data-prefetch":
+            prefetched = prefetched or interchanged
+    store = STORE_RMW if not promoted else (STORE_DEPOT if demoted else STORE_REG)
+    stage = 0
+    if promoted and interchanged:
+        stage = 2 if prefetched else 1
+    unroll = (1, 2, 4)[unrolls] if unrolls < 3 else 8
+    return VariantState(stage=stage, store=store, unroll=unroll, lsr=int(lsr), vec=int(vec))
+
+
+class VariantFamily:
+    """The precompiled variants of one benchmark and the state -> variant map.
+
+    ``knobs`` is the table exported by libpfgpu (``pf_variant_knobs``).  A
+    knob is *relevant* at a stage when it varies among that stage's variants;
+    a state selects the variant whose relevant knobs all match.  Stages above
+    the family's highest stage fall back to the highest one.
+    """
+
+    def __init__(self, bench: str, knobs: list[tuple[int, int, int, int, int]]):
+        self.bench = bench
+        self.knobs = [tuple(k) for k in knobs]
+        self.max_stage = max(k[0] for k in self.knobs)
+        self._relevant: dict[int, tuple[int, ...]] = {}
+        self._index: dict[tuple, int] = {}
+        for stage in range(self.max_stage + 1):
+            rows = [k for k in self.knobs if k[0] == stage]
+            rel = tuple(i for i in range(1, 5) if len({r[i] for r in rows}) > 1)
+            self._relevant[stage] = rel
+        for v, k in enumerate(self.knobs):
+            sig = (k[0],) + tuple(k[i] for i in self._relevant[k[0]])
+            self._index.setdefault(sig, v)
+
+    def relevant(self, stage: int) -> tuple[int, ...]:
+        return self._relevant.get(stage, ())
+
+    def select(self, state: VariantState) -> int:
+        s = state.as_tuple()
+        stage = min(s[0], self.max_stage)
+        while stage >= 0:
+            rel = self._relevant.get(stage)
+            if rel is not None:
+                sig = (stage,) + tuple(s[i] for i in rel)
+                v = self._index.get(sig)
+                if v is not None:
+                    return v
+            stage -= 1
+        raise LookupError(f"{self.bench}: no variant implements {state.key()}")
+
+    def key(self, variant: int) -> str:
+        k = self.knobs[variant]
+        rel = self.relevant(k[0])
+        parts = [f"stage={k[0]}"] + [
+            f"{KNOB_NAMES[i]}={STORE_NAMES[k[i]] if i == 1 else k[i]}" for i in rel
+        ]
+        return ",".join(parts)
+
+
+__all__ = [
+    "ALIAS_ANALYSES",
+    "BASELINE_STATE",
+    "DEFAULT_CATALOG_PASSES",
+    "STAGING_PASSES",
+    "TABLE1_PASSES",
+    "VariantFamily",
+    "VariantState",
+    "default_catalog",
+    "interpret",
+]

@@ -1,0 +1,77 @@
+"""GPU parity: every variant of every built benchmark vs the CPU oracle.
+
+Each variant runs through the C-ABI (libpfgpu.so) on the stock validation
+input and on two random inputs; its outputs must match the oracle
+(oracle/liborc.so) within rtol = 1e-4 per element with an absolute floor of
+1e-4 * max|ref| per output array (BASELINE.json north_star tolerance; the
+floor handles near-zero outputs of mixed-sign stencils and centred data).
+Input generation is checked bit-exactly against the oracle's generators.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1810_10496_b200 import registry
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+ATOL_REL = 1e-4
+
+
+def _close(got: np.ndarray, ref: np.ndarray) -> tuple[bool, float]:
+    ref64 = ref.astype(np.float64)
+    atol = ATOL_REL * float(np.max(np.abs(ref64))) if ref.size else 0.0
+    diff = np.abs(got.astype(np.float64) - ref64)
+    tol = np.maximum(atol, RTOL * np.abs(ref64))
+    worst = float(np.max(diff / np.maximum(tol, 1e-300))) if ref.size else 0.0
+    return bool(np.all(diff <= tol)), worst
+
+
+def _built(name):
+    from paper_1810_10496_b200.backend import b200
+
+    try:
+        b200.family(name)
+        return True
+    except Exception:
+        return False
+
+
+BUILT = [b for b in registry.BENCHES if _built(b)]
+
+
+@pytest.mark.parametrize("bench", BUILT)
+def test_inputs_bit_exact(bench, gpu_backend):
+    dims = registry.SIZES[bench]["validation"]
+    for stock, inst in ((True, -1), (False, 0), (False, 7)):
+        ws = gpu_backend.workspace(bench, dims, stock, inst)
+        ref = orc.generate(bench, dims, stock, gpu_backend.seed, inst)
+        for a, (name, role, _) in enumerate(ws.arrays):
+            got = ws.download(a)
+            assert np.array_equal(got, ref[a]), f"{bench} array {name} (stock={stock}, inst={inst}) differs"
+
+
+@pytest.mark.parametrize("bench", BUILT)
+def test_all_variants_match_oracle(bench, gpu_backend):
+    from paper_1810_10496_b200.backend import b200
+
+    fam = b200.family(bench)
+    dims = registry.SIZES[bench]["validation"]
+    failures = []
+    for stock, inst in ((True, -1), (False, 1)):
+        ref = orc.reference(bench, dims, stock, gpu_backend.seed, inst)
+        for v in range(len(fam.knobs)):
+            if not gpu_backend._supported(bench, v, dims):
+                continue
+            ws = gpu_backend.workspace(bench, dims, stock, inst)
+            ws.run(v, samples=1, batch=1, restore=True, flush=False)
+            outs = ws.outputs()
+            for k, (g, r) in enumerate(zip(outs, ref)):
+                ok, worst = _close(g, r)
+                if not ok:
+                    failures.append(f"v{v} [{fam.key(v)}] out{k} stock={stock}: worst/tol={worst:.3g}")
+    assert not failures, "\n".join(failures[:40])
