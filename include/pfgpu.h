@@ -119,6 +119,22 @@ int pf_run(pf_ws* ws, int variant, int samples, int batch, int restore, int flus
 int pf_run_e2e(pf_ws* ws, int variant, int samples, float* const* host_in, float* const* host_out,
                float* ms);
 
+/* Batched evaluation: the candidate evaluations of an exploration round,
+ * enqueued back to back on one stream (all workspaces on one device) with no
+ * host synchronisation between candidates.  For evaluation i:
+ *   [H2D of every non-NULL host_in[a] into ws (the runner's input upload)]
+ *   [restore in-place state] [L2 flush] start_i -> variant run -> end_i
+ *   [D2H of every output array into non-NULL host_out[a]]
+ * ms_each[i] = end_i - start_i (the variant's device time); *ms_total =
+ * first recorded event to last (the whole batch, copies included). */
+typedef struct pf_eval {
+  pf_ws* ws;
+  int variant;
+  float* const* host_in;  /* NULL or array-indexed host pointers */
+  float* const* host_out; /* NULL or array-indexed host pointers */
+} pf_eval;
+int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush_l2, float* ms_each, float* ms_total);
+
 /* ---- checking --------------------------------------------------------------
  * Device-side comparison of the output arrays of `test` against `ref`
  * (same bench and dims): element passes iff |t - r| <= max(atol, rtol*|r|)

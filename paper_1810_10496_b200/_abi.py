@@ -70,6 +70,7 @@ def _declare(lib) -> None:
         "pf_ws_array_ptr": (c_int, [c_void_p, c_int, POINTER(c_void_p)]),
         "pf_run": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, POINTER(c_float)]),
         "pf_run_e2e": (c_int, [c_void_p, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_float)]),
+        "pf_eval_batch": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_float), POINTER(c_float)]),
         "pf_compare": (c_int, [c_void_p, c_void_p, c_double, c_double, POINTER(c_double), I64P]),
         "pf_checksum": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_double)]),
         "pf_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),
@@ -101,6 +102,12 @@ def check(rc: int) -> None:
     if rc != PF_OK:
         msg = lib().pf_last_error()
         raise PfError(rc, msg.decode() if msg else "")
+
+
+class PfEval(ctypes.Structure):
+    """Mirror of ``struct pf_eval`` (include/pfgpu.h)."""
+
+    _fields_ = [("ws", c_void_p), ("variant", c_int), ("host_in", c_void_p), ("host_out", c_void_p)]
 
 
 def dims_array(dims) -> ctypes.Array:

@@ -35,17 +35,9 @@ from ctypes import byref, c_double, c_float, c_int, c_int64, c_void_p
 from pathlib import Path
 
 from .. import _abi, passmodel, registry
-from ..catalog import PhaseOrder
-from .types import (
-    Artifact,
-    Backend,
-    BackendError,
-    CompileOutcome,
-    ExecutionOutcome,
-    ExecutionStatus,
-    InputKind,
-    KernelCase,
-)
+from ..catalog import PhaseOrder, PassId
+from . import types as _own_types
+from .types import Artifact, Backend, BackendError, KernelCase
 
 ARTIFACTS_PATH = Path(__file__).resolve().parent.parent / "artifacts.json.gz"
 ARTIFACT_MAGIC = "pfgpu-artifact/1"
@@ -225,8 +217,14 @@ class B200Backend(Backend):
         min_sample_ms: float = 0.05,
         max_batch: int = 64,
         memory_budget: float = 100e9,
+        types=None,
     ):
+        """``types``: the module whose value types (Artifact, CompileOutcome,
+        ExecutionOutcome, ExecutionStatus, BackendError) this backend returns.
+        Defaults to this package's; pass ``phaseforge.backend.types`` to drive
+        the reference's unmodified engine, which compares enums by identity."""
         super().__init__()
+        self.T = types or _own_types
         self.lib = _abi.lib()
         self.device = device
         self.samples = samples
@@ -249,17 +247,19 @@ class B200Backend(Backend):
             raise ValueError(f"timeout must be positive, got {timeout}")
         self._timeouts[kernel_id] = timeout
 
-    def variant_for(self, kernel: KernelCase, order: PhaseOrder) -> tuple[str, int]:
+    def variant_for(self, kernel: KernelCase, order) -> tuple[str, int]:
         bench = registry.bench_of(kernel)
+        if not isinstance(order, PhaseOrder):  # a foreign (reference) PhaseOrder: same pass names
+            order = PhaseOrder(tuple(PassId(p.name) for p in order.passes))
         return bench, family(bench).select(passmodel.interpret(order))
 
-    def artifact(self, bench: str, variant: int) -> Artifact:
+    def artifact(self, bench: str, variant: int):
         key = (bench, variant)
         art = self._artifacts.get(key)
         if art is None:
             knobs = family(bench).knobs[variant]
             header = f"{ARTIFACT_MAGIC} bench={bench} launch=stage{knobs[0]}\n"
-            art = Artifact.from_content((header + variant_sass(bench, variant)).encode())
+            art = self.T.Artifact.from_content((header + variant_sass(bench, variant)).encode())
             self._artifacts[key] = art
         return art
 
@@ -291,42 +291,45 @@ class B200Backend(Backend):
             w.close()
         self._ws.clear()
 
-    def _crash(self, exc: _abi.PfError) -> ExecutionOutcome:
+    def _crash(self, exc: _abi.PfError):
         # A sticky CUDA error poisons the context: drop every workspace and reset.
         for w in self._ws.values():
             w.handle = None  # memory dies with the context
         self._ws.clear()
         self.lib.pf_device_reset(self.device)
-        return ExecutionOutcome(ExecutionStatus.CRASH, log=str(exc))
+        return self.T.ExecutionOutcome(self.T.ExecutionStatus.CRASH, log=str(exc))
 
     def _supported(self, bench: str, variant: int, dims) -> bool:
         rc = self.lib.pf_variant_supported(registry.bench_index(bench), variant, _abi.dims_array(dims))
         return rc == 0
 
     # ------------------------------------------------------------ Backend API
-    def compile(self, kernel: KernelCase, order: PhaseOrder) -> CompileOutcome:
+    def compile(self, kernel: KernelCase, order):
         bench, variant = self.variant_for(kernel, order)
         for text in (kernel.validation_input, kernel.measurement_input):
             _, dims = registry.parse_descriptor(text)
             if not self._supported(bench, variant, dims):
-                return CompileOutcome.codegen_failure(
+                return self.T.CompileOutcome.codegen_failure(
                     f"{bench} variant {family(bench).key(variant)} does not support {text}"
                 )
-        return CompileOutcome.success(self.artifact(bench, variant))
+        return self.T.CompileOutcome.success(self.artifact(bench, variant))
 
     def execute(
         self,
         kernel: KernelCase,
-        order: PhaseOrder,
-        artifact: Artifact,
-        input_kind: InputKind,
+        order,
+        artifact,
+        input_kind,
         random_input_index: int | None = None,
-    ) -> ExecutionOutcome:
+    ):
         bench, variant = self.variant_for(kernel, order)
         if self.artifact(bench, variant).digest != artifact.digest:
-            raise BackendError(f"artifact {artifact.digest[:12]} was not compiled from this order for {kernel.id!r}")
+            raise self.T.BackendError(
+                f"artifact {artifact.digest[:12]} was not compiled from this order for {kernel.id!r}"
+            )
         try:
-            if random_input_index is not None or input_kind is InputKind.VALIDATION:
+            # compare by value: the caller may use the reference's InputKind enum
+            if random_input_index is not None or input_kind.value == "validation":
                 _, dims = registry.parse_descriptor(kernel.validation_input)
                 stock = random_input_index is None
                 ws = self.workspace(bench, dims, stock, -1 if stock else int(random_input_index))
@@ -342,14 +345,15 @@ class B200Backend(Backend):
         except _abi.PfError as exc:
             if exc.code == _abi.PF_ECUDA:
                 return self._crash(exc)
-            raise BackendError(str(exc)) from exc
+            raise self.T.BackendError(str(exc)) from exc
 
-    def _finish(self, kernel: KernelCase, ms: float, outputs) -> ExecutionOutcome:
+    def _finish(self, kernel: KernelCase, ms: float, outputs):
         seconds = max(ms, 1e-6) * 1e-3
         limit = self._timeouts.get(kernel.id)
+        T = self.T
         if limit is not None and seconds > limit:
-            return ExecutionOutcome(ExecutionStatus.TIMEOUT, log=f"{seconds:.6f}s > timeout {limit:.6f}s")
-        return ExecutionOutcome(ExecutionStatus.VALID, wall_time=seconds, outputs=outputs)
+            return T.ExecutionOutcome(T.ExecutionStatus.TIMEOUT, log=f"{seconds:.6f}s > timeout {limit:.6f}s")
+        return T.ExecutionOutcome(T.ExecutionStatus.VALID, wall_time=seconds, outputs=outputs)
 
     def _count(self, bench: str, variant: int, dims, runs: int) -> None:
         self.device_runs += runs
@@ -379,10 +383,10 @@ class B200Backend(Backend):
         """Validation-input outputs of the empty-order (baseline) variant."""
         compiled = self.compile(kernel, PhaseOrder())
         if not compiled.is_ok:
-            raise BackendError(f"baseline compile failed for {kernel.id!r}")
-        out = self.execute(kernel, PhaseOrder(), compiled.artifact, InputKind.VALIDATION)
-        if out.status is not ExecutionStatus.VALID or out.outputs is None:
-            raise BackendError(f"baseline validation run failed for {kernel.id!r}: {out.log}")
+            raise self.T.BackendError(f"baseline compile failed for {kernel.id!r}")
+        out = self.execute(kernel, PhaseOrder(), compiled.artifact, _own_types.InputKind.VALIDATION)
+        if out.status.value != "valid" or out.outputs is None:
+            raise self.T.BackendError(f"baseline validation run failed for {kernel.id!r}: {out.log}")
         return out.outputs
 
     def time_variant(self, bench: str, dims, variant: int, samples: int | None = None) -> float:

@@ -500,6 +500,76 @@ int pf_run_e2e(pf_ws* ws, int variant, int samples, float* const* host_in, float
   return PF_OK;
 }
 
+int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush, float* ms_each, float* ms_total) {
+  if (n < 1) return fail(PF_EINVAL, "empty evaluation batch");
+  const int device = evals[0].ws->device;
+  for (int i = 0; i < n; ++i) {
+    const pf_ws* ws = evals[i].ws;
+    if (!ws || ws->device != device) return fail(PF_EINVAL, "batch workspaces must share one device");
+    if (evals[i].variant < 0 || evals[i].variant >= ws->desc->nvariants)
+      return fail(PF_EINVAL, "variant index out of range");
+    if (ws->desc->check && ws->desc->check(evals[i].variant, ws->dims) != 0)
+      return fail(PF_EINVAL, "variant does not support these dims");
+  }
+  if (int rc = set_device(device)) return rc;
+  // Everything goes on the first workspace's stream; the others must be idle.
+  for (int i = 0; i < n; ++i) PF_CUDA(cudaStreamSynchronize(evals[i].ws->stream));
+  cudaStream_t st = evals[0].ws->stream;
+  thread_local std::vector<cudaEvent_t> pool;
+  while ((int)pool.size() < 2 * n + 2) {
+    cudaEvent_t e;
+    PF_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  cudaEvent_t first = pool[2 * n], last = pool[2 * n + 1];
+  PF_CUDA(cudaEventRecord(first, st));
+  for (int i = 0; i < n; ++i) {
+    pf_ws* ws = evals[i].ws;
+    const BenchDesc* d = ws->desc;
+    if (evals[i].host_in) {
+      for (int a = 0; a < d->narrays; ++a) {
+        if (!evals[i].host_in[a] || d->arrays[a].role == OUT) continue;
+        const size_t bytes = ws->elems[a] * sizeof(float);
+        PF_CUDA(cudaMemcpyAsync(ws->a.p[a], evals[i].host_in[a], bytes, cudaMemcpyHostToDevice, st));
+        if (ws->pristine[a])
+          PF_CUDA(cudaMemcpyAsync(ws->pristine[a], ws->a.p[a], bytes, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    if (restore) {
+      for (int a = 0; a < d->narrays; ++a) {
+        const size_t bytes = ws->elems[a] * sizeof(float);
+        if (d->arrays[a].role == INOUT)
+          PF_CUDA(cudaMemcpyAsync(ws->a.p[a], ws->pristine[a], bytes, cudaMemcpyDeviceToDevice, st));
+        else if (d->arrays[a].role == OUT)
+          PF_CUDA(cudaMemsetAsync(ws->a.p[a], 0, bytes, st));
+      }
+    }
+    if (flush)
+      if (int rc = flush_l2(device, st)) return rc;
+    PF_CUDA(cudaEventRecord(pool[2 * i], st));
+    d->run[evals[i].variant](*ws, st);
+    PF_CUDA(cudaGetLastError());
+    PF_CUDA(cudaEventRecord(pool[2 * i + 1], st));
+    if (evals[i].host_out) {
+      for (int a = 0; a < d->narrays; ++a)
+        if (d->arrays[a].is_output && evals[i].host_out[a])
+          PF_CUDA(cudaMemcpyAsync(evals[i].host_out[a], ws->a.p[a], ws->elems[a] * sizeof(float),
+                                  cudaMemcpyDeviceToHost, st));
+    }
+  }
+  PF_CUDA(cudaEventRecord(last, st));
+  PF_CUDA(cudaEventSynchronize(last));
+  for (int i = 0; i < n; ++i) {
+    float t = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&t, pool[2 * i], pool[2 * i + 1]));
+    if (ms_each) ms_each[i] = t;
+  }
+  float tot = 0.f;
+  PF_CUDA(cudaEventElapsedTime(&tot, first, last));
+  if (ms_total) *ms_total = tot;
+  return PF_OK;
+}
+
 int pf_compare(pf_ws* test, pf_ws* ref, double rtol, double atol_rel, double* max_err, int64_t* nbad) {
   if (test->bench != ref->bench) return fail(PF_EINVAL, "workspaces hold different benchmarks");
   for (int i = 0; i < kMaxDims; ++i)

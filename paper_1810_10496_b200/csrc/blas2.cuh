@@ -1,0 +1,290 @@
+// Shared kernels for the memory-bound BLAS-2 set (ATAX, BICG, MVT, GESUMMV).
+//
+// stage 0  PolyBench/GPU shapes: thread-per-row loops (uncoalesced: a warp
+//          touches 32 rows) and thread-per-column loops (coalesced), with the
+//          store / unroll / lsr / vec knobs.
+// stage 1  warp-per-row dot products (coalesced 512-byte row segments,
+//          shuffle reduction) and row-split column products (enough CTAs to
+//          fill 148 SMs, partials merged with vector atomics).
+// stage 2  one persistent pass over A: every A row is loaded from HBM once
+//          into registers and feeds both the row dot product (block
+//          reduction) and the column accumulation (register partials,
+//          merged once per CTA) -- 4N^2 compulsory bytes instead of 8N^2.
+#pragma once
+#include "pf_common.cuh"
+
+#include <algorithm>
+
+namespace pf {
+
+// ---------------------------------------------------------------- stage 0
+// dst (+)= sum_j A[row*lda + j] * v[j], j in [0, n).  zero: start from 0.
+template <int kStore, int kUnroll, int kLsr, int kVec>
+__device__ __forceinline__ void s0_row_dot(float* dst, const float* A, int lda, int row, const float* v, int n,
+                                           bool zero) {
+  Acc<kStore> acc;
+  acc.init(dst, zero ? 0.0f : *dst);
+  if constexpr (kVec) {
+    const float4* a4 = reinterpret_cast<const float4*>(A + (size_t)row * lda);
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    PF_UNROLL_IMPL(kUnroll)
+    for (int q = 0; q < n / 4; ++q) {
+      float4 a = a4[q], b = v4[q];
+      acc.add(dst, a.x * b.x);
+      acc.add(dst, a.y * b.y);
+      acc.add(dst, a.z * b.z);
+      acc.add(dst, a.w * b.w);
+    }
+  } else if constexpr (kLsr) {
+    const float* pa = A + (size_t)row * lda;
+    const float* pv = v;
+    PF_UNROLL_IMPL(kUnroll)
+    for (int j = n; j > 0; --j) acc.add(dst, *pa++ * *pv++);
+  } else {
+    PF_UNROLL_IMPL(kUnroll)
+    for (int j = 0; j < n; j++) acc.add(dst, A[row * lda + j] * v[j]);
+  }
+  acc.finish(dst);
+}
+
+// dst[col+e] (+)= sum_i A[i*lda + col+e] * v[i], i in [0, m); e < (kVec ? 4 : 1).
+template <int kStore, int kUnroll, int kLsr, int kVec>
+__device__ __forceinline__ void s0_col_dot(float* dst, const float* A, int lda, int col, const float* v, int m,
+                                           bool zero) {
+  constexpr int W = kVec ? 4 : 1;
+  Acc<kStore> acc[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) acc[e].init(dst + e, zero ? 0.0f : dst[e]);
+  if constexpr (kVec) {
+    PF_UNROLL_IMPL(kUnroll)
+    for (int i = 0; i < m; i++) {
+      float4 a = *reinterpret_cast<const float4*>(A + (size_t)i * lda + col);
+      float vi = v[i];
+      acc[0].add(dst + 0, a.x * vi);
+      acc[1].add(dst + 1, a.y * vi);
+      acc[2].add(dst + 2, a.z * vi);
+      acc[3].add(dst + 3, a.w * vi);
+    }
+  } else if constexpr (kLsr) {
+    const float* pa = A + col;
+    const float* pv = v;
+    PF_UNROLL_IMPL(kUnroll)
+    for (int i = m; i > 0; --i) {
+      acc[0].add(dst, *pa * *pv++);
+      pa += lda;
+    }
+  } else {
+    PF_UNROLL_IMPL(kUnroll)
+    for (int i = 0; i < m; i++) acc[0].add(dst, A[i * lda + col] * v[i]);
+  }
+#pragma unroll
+  for (int e = 0; e < W; ++e) acc[e].finish(dst + e);
+}
+
+// ---------------------------------------------------------------- stage 1
+// Warp-per-row: out[row] = (init ? init[row] : 0) + sum_j A[row][j] v[j]
+template <BenchId Bn, int V, int kUnroll, int kVec>
+__global__ void __launch_bounds__(256) s1_row_dot(const float* __restrict__ A, int lda, const float* __restrict__ v,
+                                                  int n, int rows, const float* init, float* out) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += warps) {
+    const float* a = A + (size_t)row * lda;
+    float s = 0.f;
+    if constexpr (kVec) {
+      const float4* a4 = reinterpret_cast<const float4*>(a);
+      const float4* v4 = reinterpret_cast<const float4*>(v);
+      PF_UNROLL_IMPL(kUnroll)
+      for (int q = lane; q < n / 4; q += 32) {
+        float4 x = __ldg(a4 + q), y = __ldg(v4 + q);
+        s = fmaf(x.x, y.x, s);
+        s = fmaf(x.y, y.y, s);
+        s = fmaf(x.z, y.z, s);
+        s = fmaf(x.w, y.w, s);
+      }
+    } else {
+      PF_UNROLL_IMPL(kUnroll)
+      for (int j = lane; j < n; j += 32) s = fmaf(__ldg(a + j), __ldg(v + j), s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) out[row] = (init ? init[row] : 0.f) + s;
+  }
+}
+
+// Row-split column product: out[col] += sum_{i in split} A[i][col] v[i]
+// (out holds its initial value; partials are added atomically).
+template <BenchId Bn, int V, int kUnroll, int kVec>
+__global__ void __launch_bounds__(256) s1_col_dot(const float* __restrict__ A, int lda, const float* __restrict__ v,
+                                                  int m, int cols, int rows_per_split, float* out) {
+  constexpr int W = kVec ? 4 : 1;
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * W;
+  if (col >= cols) return;
+  const int i0 = blockIdx.y * rows_per_split;
+  const int i1 = min(m, i0 + rows_per_split);
+  float s[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) s[e] = 0.f;
+  PF_UNROLL_IMPL(kUnroll)
+  for (int i = i0; i < i1; ++i) {
+    const float vi = __ldg(v + i);
+    if constexpr (kVec) {
+      float4 a = __ldg(reinterpret_cast<const float4*>(A + (size_t)i * lda + col));
+      s[0] = fmaf(a.x, vi, s[0]);
+      s[1] = fmaf(a.y, vi, s[1]);
+      s[2] = fmaf(a.z, vi, s[2]);
+      s[3] = fmaf(a.w, vi, s[3]);
+    } else {
+      s[0] = fmaf(__ldg(A + (size_t)i * lda + col), vi, s[0]);
+    }
+  }
+  if constexpr (kVec)
+    atomicAdd(reinterpret_cast<float4*>(out + col), make_float4(s[0], s[1], s[2], s[3]));
+  else
+    atomicAdd(out + col, s[0]);
+}
+
+template <BenchId Bn, int V, int kUnroll, int kVec>
+inline void launch_s1_row_dot(const float* A, int lda, const float* v, int n, int rows, const float* init, float* out,
+                              cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(((int64_t)rows + 7) / 8, 148 * 16);
+  s1_row_dot<Bn, V, kUnroll, kVec><<<blocks, 256, 0, s>>>(A, lda, v, n, rows, init, out);
+}
+
+template <BenchId Bn, int V, int kUnroll, int kVec>
+inline void launch_s1_col_dot(const float* A, int lda, const float* v, int m, int cols, float* out, cudaStream_t s) {
+  constexpr int W = kVec ? 4 : 1;
+  const int gx = (int)cdiv(cols, 256 * W);
+  int splits = (int)cdiv(148 * 4, gx);
+  splits = std::max(1, std::min(splits, (m + 63) / 64));
+  const int rps = (int)cdiv(m, splits);
+  splits = (int)cdiv(m, rps);
+  s1_col_dot<Bn, V, kUnroll, kVec><<<dim3(gx, splits), 256, 0, s>>>(A, lda, v, m, cols, rps, out);
+}
+
+// ---------------------------------------------------------------- stage 2
+// One pass over A[rows][cols] (cols % 4 == 0).  Thread t owns the float4
+// column chunks q = t + T*c (c < C4).  Per row r:
+//   dot_r = sum_j A[r][j] * xv[j]                  (if rowout)
+//   rowout[r] = (rowinit ? rowinit[r] : 0) + dot_r
+//   colacc[j] += A[r][j] * (colcoef ? colcoef[r] : dot_r)   (if colout)
+// xv is staged in shared memory; the next row is prefetched into registers
+// while the current one is reduced; per-CTA column partials are merged with
+// float4 atomics at the end (colout holds its initial value).
+struct FusedArgs {
+  const float* A;
+  int rows, cols;
+  const float* xv;
+  float* rowout;
+  const float* rowinit;
+  const float* colcoef;
+  float* colout;
+};
+
+constexpr int kFusedThreads = 512;
+
+template <BenchId Bn, int V, int C4>
+__global__ void __launch_bounds__(kFusedThreads, 1) s2_fused(FusedArgs p) {
+  extern __shared__ float4 xs4[];
+  __shared__ float red[2][kFusedThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nq = p.cols >> 2;
+  const bool do_row = p.rowout != nullptr;
+  const bool do_col = p.colout != nullptr;
+  if (do_row)
+    for (int q = t; q < nq; q += kFusedThreads) xs4[q] = __ldg(reinterpret_cast<const float4*>(p.xv) + q);
+  __syncthreads();
+  float4 acc[C4], cur[C4], nxt[C4];
+#pragma unroll
+  for (int c = 0; c < C4; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto load_row = [&](int r, float4 (&dst)[C4]) {
+    const float4* a4 = reinterpret_cast<const float4*>(p.A + (size_t)r * p.cols);
+#pragma unroll
+    for (int c = 0; c < C4; ++c) {
+      const int q = t + kFusedThreads * c;
+      dst[c] = q < nq ? __ldcs(a4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  int r = blockIdx.x;
+  if (r < p.rows) load_row(r, cur);
+  int buf = 0;
+  for (; r < p.rows; r += gridDim.x) {
+    const int rn = r + gridDim.x;
+    if (rn < p.rows) load_row(rn, nxt);
+    float coef = 0.f;
+    if (do_row) {
+      float d = 0.f;
+#pragma unroll
+      for (int c = 0; c < C4; ++c) {
+        const int q = t + kFusedThreads * c;
+        if (q < nq) {
+          float4 x = xs4[q];
+          d = fmaf(cur[c].x, x.x, d);
+          d = fmaf(cur[c].y, x.y, d);
+          d = fmaf(cur[c].z, x.z, d);
+          d = fmaf(cur[c].w, x.w, d);
+        }
+      }
+      d = warp_sum(d);
+      if (lane == 0) red[buf][warp] = d;
+      __syncthreads();
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < kFusedThreads / 32; ++w) tot += red[buf][w];
+      buf ^= 1;
+      if (t == 0) p.rowout[r] = (p.rowinit ? p.rowinit[r] : 0.f) + tot;
+      coef = tot;
+    }
+    if (do_col) {
+      if (p.colcoef) coef = __ldg(p.colcoef + r);
+#pragma unroll
+      for (int c = 0; c < C4; ++c) {
+        acc[c].x = fmaf(cur[c].x, coef, acc[c].x);
+        acc[c].y = fmaf(cur[c].y, coef, acc[c].y);
+        acc[c].z = fmaf(cur[c].z, coef, acc[c].z);
+        acc[c].w = fmaf(cur[c].w, coef, acc[c].w);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C4; ++c) cur[c] = nxt[c];
+  }
+  if (do_col) {
+#pragma unroll
+    for (int c = 0; c < C4; ++c) {
+      const int q = t + kFusedThreads * c;
+      if (q < nq) atomicAdd(reinterpret_cast<float4*>(p.colout) + q, acc[c]);
+    }
+  }
+}
+
+inline int fused_c4(int cols) { return (int)cdiv(cols / 4, kFusedThreads); }
+
+// Supported when cols % 4 == 0, the column vector fits in shared memory and
+// C4 is one of the instantiated widths.
+inline bool fused_supported(int64_t rows, int64_t cols) {
+  if (rows < 1 || cols < 4 || cols % 4) return false;
+  if (cols * 4 > 200 * 1024) return false;
+  return fused_c4((int)cols) <= 8;
+}
+
+template <BenchId Bn, int V, int C4>
+inline void launch_fused_c4(const FusedArgs& p, cudaStream_t s) {
+  const size_t smem = (size_t)p.cols * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(s2_fused<Bn, V, C4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  int grid = std::min(p.rows, 148);
+  s2_fused<Bn, V, C4><<<grid, kFusedThreads, smem, s>>>(p);
+}
+
+template <BenchId Bn, int V>
+inline void launch_fused(const FusedArgs& p, cudaStream_t s) {
+  const int c4 = fused_c4(p.cols);
+  if (c4 <= 1) launch_fused_c4<Bn, V, 1>(p, s);
+  else if (c4 <= 2) launch_fused_c4<Bn, V, 2>(p, s);
+  else if (c4 <= 4) launch_fused_c4<Bn, V, 4>(p, s);
+  else launch_fused_c4<Bn, V, 8>(p, s);
+}
+
+}  // namespace pf
