@@ -1,0 +1,222 @@
+// GRAMSCHM (PolyBench/GPU gramschmidt.cu): modified Gram-Schmidt QR of an
+// M x N matrix A (A is overwritten; outputs A, R, Q).
+//
+// Baseline, per column k (3N launches): gramschmidt_kernel1 with a single
+// thread summing the column norm, kernel2 normalising Q[:,k], kernel3 one
+// thread per trailing column j computing R[k][j] (accumulated in global
+// memory inside the i loop) then updating A[:,j].  Paper: 1.49x over CUDA
+// from store motion.  Stage 1: block-parallel norm fused
+// with the Q column, the R row as a split-i vector-matrix product, and a
+// 2-D elementwise trailing update; stage 2: the stage-1 sequence captured as
+// one CUDA graph.
+//
+// Input deviation (documented): PolyBench's A = (i+1)(j+1)/(M+1)
+// is rank 1; here A = U[0,1) + N*I so the factorisation is well conditioned.
+#include "pf_common.cuh"
+
+#include <algorithm>
+
+namespace pf {
+namespace {
+
+constexpr auto kTab = make_variants<2, 1, 1, 1>();
+constexpr int kNV = sizeof(kTab.v) / sizeof(Knobs);
+
+struct Init {
+  int64_t n;
+  uint64_t key;
+  __device__ float operator()(int64_t idx) const {
+    float u = unit_float(key, idx);
+    if (idx / n == idx % n) u = fadd(u, i2f(n));
+    return u;
+  }
+};
+
+void launch_init(float* out, int array, int64_t n, const Dims& d, int stock, uint64_t seed, int64_t inst,
+                 cudaStream_t s) {
+  const uint64_t key = stock ? stream_key(1729, B_GRAMSCHM, array, -2) : stream_key(seed, B_GRAMSCHM, array, inst);
+  launch_init_with(out, n, Init{d.d[1], key}, s);
+}
+
+// ---- stage 0 (PolyBench shape)
+template <BenchId Bn, int V>
+__global__ void gs_k1(const float* a, float* r, int m, int n, int k) {
+  constexpr Knobs K = kTab.v[V];
+  if (threadIdx.x == 0) {
+    float nrm = 0.0f;
+    if constexpr (K.lsr) {
+      const float* p = a + k;
+      PF_UNROLL_IMPL(K.unroll)
+      for (int i = m; i > 0; --i) {
+        nrm += *p * *p;
+        p += n;
+      }
+    } else {
+      PF_UNROLL_IMPL(K.unroll)
+      for (int i = 0; i < m; i++) nrm += a[i * n + k] * a[i * n + k];
+    }
+    r[k * n + k] = sqrtf(nrm);
+  }
+}
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) gs_k2(const float* a, const float* r, float* q, int m, int n, int k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) q[i * n + k] = a[i * n + k] / r[k * n + k];
+}
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) gs_k3(float* a, float* r, const float* q, int m, int n, int k) {
+  constexpr Knobs K = kTab.v[V];
+  constexpr int W = K.vec ? 4 : 1;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * W;
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const int j = j0 + e;
+    if ((j > k) && (j < n)) {
+      float* dst = &r[k * n + j];
+      Acc<K.store> acc;
+      acc.init(dst, 0.0f);
+      if constexpr (K.lsr) {
+        const float* pq = q + k;
+        const float* pa = a + j;
+        PF_UNROLL_IMPL(K.unroll)
+        for (int i = m; i > 0; --i) {
+          acc.add(dst, *pq * *pa);
+          pq += n;
+          pa += n;
+        }
+      } else {
+        PF_UNROLL_IMPL(K.unroll)
+        for (int i = 0; i < m; i++) acc.add(dst, q[i * n + k] * a[i * n + j]);
+      }
+      acc.finish(dst);
+      PF_UNROLL_IMPL(K.unroll)
+      for (int i = 0; i < m; i++) a[i * n + j] -= q[i * n + k] * acc.get(dst);
+    }
+  }
+}
+
+// ---- stage 1
+// Column norm with a block reduction, then Q[:,k] = A[:,k] / R[k][k].
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(1024) gs_norm_q(const float* __restrict__ a, float* r, float* q, int m, int n,
+                                                  int k) {
+  __shared__ float part[32];
+  __shared__ float rkk;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const float v = a[(size_t)i * n + k];
+    s = fmaf(v, v, s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) {
+      rkk = sqrtf(t);
+      r[(size_t)k * n + k] = rkk;
+    }
+  }
+  __syncthreads();
+  const float inv = rkk;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) q[(size_t)i * n + k] = a[(size_t)i * n + k] / inv;
+}
+
+// R[k][j] += sum_{i in split} Q[i][k] A[i][j], j > k (R row k starts at 0).
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) gs_rrow(const float* __restrict__ a, float* r, const float* __restrict__ q,
+                                               int m, int n, int k, int rows_per_split) {
+  const int j = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int i0 = blockIdx.y * rows_per_split, i1 = min(m, i0 + rows_per_split);
+  float s0 = 0.f, s1 = 0.f;
+  int i = i0;
+  for (; i + 1 < i1; i += 2) {
+    s0 = fmaf(__ldg(q + (size_t)i * n + k), a[(size_t)i * n + j], s0);
+    s1 = fmaf(__ldg(q + (size_t)(i + 1) * n + k), a[(size_t)(i + 1) * n + j], s1);
+  }
+  if (i < i1) s0 = fmaf(__ldg(q + (size_t)i * n + k), a[(size_t)i * n + j], s0);
+  atomicAdd(r + (size_t)k * n + j, s0 + s1);
+}
+
+// A[i][j] -= Q[i][k] R[k][j] for j > k.
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) gs_update(float* a, const float* __restrict__ r, const float* __restrict__ q,
+                                                 int m, int n, int k) {
+  const int j = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (j >= n || i >= m) return;
+  a[(size_t)i * n + j] -= __ldg(q + (size_t)i * n + k) * __ldg(r + (size_t)k * n + j);
+}
+
+template <BenchId Bn, int V>
+void s1_sequence(Workspace& ws, cudaStream_t s) {
+  const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
+  float* A = ws.a.p[0];
+  float* R = ws.a.p[1];
+  float* Q = ws.a.p[2];
+  for (int k = 0; k < n; ++k) {
+    gs_norm_q<Bn, V><<<1, 1024, 0, s>>>(A, R, Q, m, n, k);
+    const int cols = n - k - 1;
+    if (cols <= 0) continue;
+    const int gx = (int)cdiv(cols, 256);
+    int splits = std::max(1, std::min((int)cdiv(148 * 2, gx), (m + 127) / 128));
+    const int rps = (int)cdiv(m, splits);
+    splits = (int)cdiv(m, rps);
+    gs_rrow<Bn, V><<<dim3(gx, splits), 256, 0, s>>>(A, R, Q, m, n, k, rps);
+    gs_update<Bn, V><<<dim3(cdiv(cols, 32), cdiv(m, 8)), dim3(32, 8), 0, s>>>(A, R, Q, m, n, k);
+  }
+}
+
+template <int V>
+struct Run {
+  static void run(Workspace& ws, cudaStream_t s) {
+    constexpr Knobs K = kTab.v[V];
+    const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
+    float* A = ws.a.p[0];
+    float* R = ws.a.p[1];
+    float* Q = ws.a.p[2];
+    if constexpr (K.stage == 0) {
+      for (int k = 0; k < n; ++k) {
+        gs_k1<B_GRAMSCHM, V><<<1, kB1, 0, s>>>(A, R, m, n, k);
+        gs_k2<B_GRAMSCHM, V><<<cdiv(m, kB1), kB1, 0, s>>>(A, R, Q, m, n, k);
+        gs_k3<B_GRAMSCHM, V><<<cdiv(n, kB1 * (K.vec ? 4 : 1)), kB1, 0, s>>>(A, R, Q, m, n, k);
+      }
+    } else if constexpr (K.stage == 1) {
+      s1_sequence<B_GRAMSCHM, V>(ws, s);
+    } else {
+      cudaGraphExec_t g = cached_graph(ws, V, &s1_sequence<B_GRAMSCHM, V>);
+      cudaGraphLaunch(g, s);
+    }
+  }
+};
+
+constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{});
+
+int64_t elems(int a, const Dims& d) { return a == 1 ? d.d[1] * d.d[1] : d.d[0] * d.d[1]; }
+int64_t launches(int v, const Dims& d) {
+  const int st = kTab.v[v].stage;
+  return st == 0 ? 3 * d.d[1] : 3 * d.d[1] - 2;
+}
+double alg_bytes(const Dims& d) {
+  const double m = d.d[0], n = d.d[1];
+  return 4.0 * (2.0 * m * n + n * n + m * n);
+}
+double alg_flops(const Dims& d) { return 2.0 * (double)d.d[0] * d.d[1] * d.d[1]; }
+int check(int v, const Dims& d) {
+  if (kTab.v[v].vec && d.d[1] % 4) return 1;
+  return 0;
+}
+
+const BenchDesc kDesc = {
+    "GRAMSCHM", 2, {"m", "n"}, 3,
+    {{"A", INOUT, 1}, {"R", OUT, 1}, {"Q", OUT, 1}},
+    elems, launch_init, kNV, kTab.v, kRun.f, launches, alg_bytes, alg_flops, check,
+};
+Registrar reg(B_GRAMSCHM, &kDesc);
+
+}  // namespace
+}  // namespace pf

@@ -1,0 +1,118 @@
+// SYR2K (PolyBench/GPU syr2k.cu): C = beta*C + alpha*A*B^T + alpha*B*A^T.
+//
+// Baseline: syr2k_kernel, one thread per C element, both products
+// accumulated into c[i][j] in global memory inside the k loop.  Paper: 1.99x
+// over CUDA / 2.05x over OpenCL from store motion, unrolling and outlining
+// (PAPER.md:410-412).  Stage 1: tiled SIMT with both products in one
+// accumulator; stage 2: tcgen05 3xTF32 on the K-concatenation [A B][B A]^T.
+#include "pf_common.cuh"
+#include "simt_gemm.cuh"
+#include "tc_gemm.cuh"
+
+namespace pf {
+namespace {
+
+constexpr float kAlpha = 12435.0f;
+constexpr float kBeta = 4546.0f;
+
+constexpr auto kTab = make_variants<2, 1, 1, 1>();
+constexpr int kNV = sizeof(kTab.v) / sizeof(Knobs);
+
+struct Init {
+  int array;
+  int64_t n, m;
+  int stock;
+  uint64_t key;
+  __device__ float operator()(int64_t idx) const {
+    if (!stock) return unit_float(key, idx);
+    if (array == 0) return fdiv(fadd(fmul(i2f(idx / m), i2f(idx % m)), 1.0f), i2f(n));  // A = (i*k+1)/N
+    if (array == 1) return fdiv(fadd(fmul(i2f(idx / m), i2f(idx % m)), 2.0f), i2f(n));  // B = (i*k+2)/N
+    return fdiv(fadd(fmul(i2f(idx / n), i2f(idx % n)), 2.0f), i2f(n));                  // C = (i*j+2)/N
+  }
+};
+
+void launch_init(float* out, int array, int64_t n, const Dims& d, int stock, uint64_t seed, int64_t inst,
+                 cudaStream_t s) {
+  launch_init_with(out, n, Init{array, d.d[0], d.d[1], stock, stream_key(seed, B_SYR2K, array, inst)}, s);
+}
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) syr2k_s0(const float* a, const float* b, float* c, int n, int m) {
+  constexpr Knobs K = kTab.v[V];
+  constexpr int U = K.unroll;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= n || j >= n) return;
+  float* dst = &c[i * n + j];
+  Acc<K.store> acc;
+  acc.init(dst, *dst * kBeta);
+  if constexpr (K.vec) {
+    const float4* ai = reinterpret_cast<const float4*>(a + (size_t)i * m);
+    const float4* bi = reinterpret_cast<const float4*>(b + (size_t)i * m);
+    const float4* aj = reinterpret_cast<const float4*>(a + (size_t)j * m);
+    const float4* bj = reinterpret_cast<const float4*>(b + (size_t)j * m);
+    PF_UNROLL_IMPL(U)
+    for (int q = 0; q < m / 4; ++q) {
+      const float4 x = ai[q], y = bj[q], z = bi[q], w = aj[q];
+      acc.add(dst, kAlpha * x.x * y.x + kAlpha * z.x * w.x);
+      acc.add(dst, kAlpha * x.y * y.y + kAlpha * z.y * w.y);
+      acc.add(dst, kAlpha * x.z * y.z + kAlpha * z.z * w.z);
+      acc.add(dst, kAlpha * x.w * y.w + kAlpha * z.w * w.w);
+    }
+  } else if constexpr (K.lsr) {
+    const float* pai = a + (size_t)i * m;
+    const float* pbi = b + (size_t)i * m;
+    const float* paj = a + (size_t)j * m;
+    const float* pbj = b + (size_t)j * m;
+    PF_UNROLL_IMPL(U)
+    for (int k = m; k > 0; --k) acc.add(dst, kAlpha * *pai++ * *pbj++ + kAlpha * *pbi++ * *paj++);
+  } else {
+    PF_UNROLL_IMPL(U)
+    for (int k = 0; k < m; k++)
+      acc.add(dst, kAlpha * a[i * m + k] * b[j * m + k] + kAlpha * b[i * m + k] * a[j * m + k]);
+  }
+  acc.finish(dst);
+}
+
+template <int V>
+struct Run {
+  static void run(Workspace& ws, cudaStream_t s) {
+    constexpr Knobs K = kTab.v[V];
+    const int n = (int)ws.dims.d[0], m = (int)ws.dims.d[1];
+    const float* A = ws.a.p[0];
+    const float* B = ws.a.p[1];
+    float* C = ws.a.p[2];
+    if constexpr (K.stage == 0) {
+      dim3 block(kBX, kBY), grid(cdiv(n, kBX), cdiv(n, kBY));
+      syr2k_s0<B_SYR2K, V><<<grid, block, 0, s>>>(A, B, C, n, m);
+    } else if constexpr (K.stage == 1) {
+      launch_simt_gemm<B_SYR2K, V, false, true, true>(
+          SimtGemmArgs{n, n, m, kAlpha, kBeta, A, m, B, m, B, A, C, n, C, n, 0}, s);
+    } else {
+      launch_tc_gemm<B_SYR2K, V>(
+          ws, TcGemmArgs{n, n, m, kAlpha, kBeta, A, m, false, B, m, true, B, A, C, n, C, n, 0}, s);
+    }
+  }
+};
+
+constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{});
+
+int64_t elems(int a, const Dims& d) { return a <= 1 ? d.d[0] * d.d[1] : d.d[0] * d.d[0]; }
+int64_t launches(int v, const Dims&) { return kTab.v[v].stage == 2 ? tc_gemm_launches(true) : 1; }
+double alg_bytes(const Dims& d) { return 4.0 * (2.0 * d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }
+double alg_flops(const Dims& d) { return 4.0 * (double)d.d[0] * d.d[0] * d.d[1]; }
+int check(int v, const Dims& d) {
+  const Knobs& k = kTab.v[v];
+  if (k.stage == 0 && k.vec && d.d[1] % 4) return 1;
+  return 0;
+}
+
+const BenchDesc kDesc = {
+    "SYR2K", 2, {"n", "m"}, 3,
+    {{"A", IN, 0}, {"B", IN, 0}, {"C", INOUT, 1}},
+    elems, launch_init, kNV, kTab.v, kRun.f, launches, alg_bytes, alg_flops, check,
+};
+Registrar reg(B_SYR2K, &kDesc);
+
+}  // namespace
+}  // namespace pf

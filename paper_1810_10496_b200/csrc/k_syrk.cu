@@ -1,0 +1,78 @@
+// SYRK (PolyBench/GPU syrk.cu): C = beta*C + alpha*A*A^T over the full N x N.
+//
+// Baseline: syrk_kernel, one thread per C element (j = x), `c *= beta` then
+// `c += alpha*a[i][k]*a[j][k]` in global memory inside the k loop; a[j][k]
+// strides M across the warp.  Paper: 1.14x over OpenCL, none over CUDA
+// (PAPER.md:414-416).  Stage 1: tiled SIMT; stage 2: tcgen05 3xTF32 with
+// both operands K-major.
+#include "pf_common.cuh"
+#include "dense_s0.cuh"
+#include "simt_gemm.cuh"
+#include "tc_gemm.cuh"
+
+namespace pf {
+namespace {
+
+constexpr float kAlpha = 12435.0f;
+constexpr float kBeta = 4546.0f;
+
+constexpr auto kTab = make_variants<2, 1, 1, 1>();
+constexpr int kNV = sizeof(kTab.v) / sizeof(Knobs);
+
+struct Init {
+  int array;
+  int64_t n, m;
+  int stock;
+  uint64_t key;
+  __device__ float operator()(int64_t idx) const {
+    if (!stock) return unit_float(key, idx);
+    if (array == 0) return fdiv(fmul(i2f(idx / m), i2f(idx % m)), i2f(n));        // A = i*k/N
+    return fdiv(fadd(fmul(i2f(idx / n), i2f(idx % n)), 2.0f), i2f(n));            // C = (i*j+2)/N
+  }
+};
+
+void launch_init(float* out, int array, int64_t n, const Dims& d, int stock, uint64_t seed, int64_t inst,
+                 cudaStream_t s) {
+  launch_init_with(out, n, Init{array, d.d[0], d.d[1], stock, stream_key(seed, B_SYRK, array, inst)}, s);
+}
+
+template <int V>
+struct Run {
+  static void run(Workspace& ws, cudaStream_t s) {
+    constexpr Knobs K = kTab.v[V];
+    const int n = (int)ws.dims.d[0], m = (int)ws.dims.d[1];
+    const float* A = ws.a.p[0];
+    float* C = ws.a.p[1];
+    if constexpr (K.stage == 0) {
+      launch_s0_mm<B_SYRK, V, K.store, K.unroll, K.lsr, K.vec, true>(A, m, A, m, C, n, n, n, m, kAlpha, 1, kBeta, s);
+    } else if constexpr (K.stage == 1) {
+      launch_simt_gemm<B_SYRK, V, false, true, false>(
+          SimtGemmArgs{n, n, m, kAlpha, kBeta, A, m, A, m, nullptr, nullptr, C, n, C, n, 0}, s);
+    } else {
+      launch_tc_gemm<B_SYRK, V>(
+          ws, TcGemmArgs{n, n, m, kAlpha, kBeta, A, m, false, A, m, true, nullptr, nullptr, C, n, C, n, 0}, s);
+    }
+  }
+};
+
+constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{});
+
+int64_t elems(int a, const Dims& d) { return a == 0 ? d.d[0] * d.d[1] : d.d[0] * d.d[0]; }
+int64_t launches(int v, const Dims&) { return kTab.v[v].stage == 2 ? tc_gemm_launches(false) : 1; }
+double alg_bytes(const Dims& d) { return 4.0 * ((double)d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }
+double alg_flops(const Dims& d) { return 2.0 * (double)d.d[0] * d.d[0] * d.d[1]; }
+int check(int v, const Dims& d) {
+  const Knobs& k = kTab.v[v];
+  if (k.stage == 0 && k.vec && d.d[1] % 4) return 1;
+  return 0;
+}
+
+const BenchDesc kDesc = {
+    "SYRK", 2, {"n", "m"}, 2,
+    {{"A", IN, 0}, {"C", INOUT, 1}},
+    elems, launch_init, kNV, kTab.v, kRun.f, launches, alg_bytes, alg_flops, check,
+};
+Registrar reg(B_SYRK, &kDesc);
+
+}  // namespace
+}  // namespace pf

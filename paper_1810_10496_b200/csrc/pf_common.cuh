@@ -105,6 +105,10 @@ struct Workspace {
   float* ensure_scratch(size_t bytes);  // defined in abi.cu; only called outside timed regions' first use
 };
 
+// Graph-staged variants: capture `body` once per (workspace, key) and return
+// the executable graph (abi.cu).  Launch with cudaGraphLaunch(exec, stream).
+cudaGraphExec_t cached_graph(Workspace& ws, int key, void (*body)(Workspace&, cudaStream_t));
+
 // Registration: each k_*.cu module registers its descriptor at load time.
 void register_bench(int id, const BenchDesc* desc);
 struct Registrar {
