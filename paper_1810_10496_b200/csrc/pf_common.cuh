@@ -173,7 +173,9 @@ struct Stage0 {
   static constexpr int kCount = 1 + 3 * 4 * 2 * kNVec;
 };
 
-constexpr int kUnrolls[4] = {1, 2, 4, 8};
+// LLVM-path unroll ladder: the paper's phase-ordered PTX is unrolled x2 without a
+// loop-unroll pass; each loop-unroll doubles it.
+constexpr int kUnrolls[4] = {2, 4, 8, 16};
 
 template <size_t N>
 struct VariantTable {

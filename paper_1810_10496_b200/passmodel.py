@@ -22,11 +22,13 @@ i.e. the nvcc/PolyBench code shape):
   re-promotes them.  A promoted accumulator left demoted is the
   ``__local_depot`` shape of CORR/COVAR (PAPER.md:388-390);
 * ``loop-reduce`` strength-reduces address arithmetic (PAPER.md:329-358);
-* each ``loop-unroll`` doubles the unroll factor of the reduction loop
-  (1, 2, 4, then 8); without it an LLVM-compiled loop stays rolled;
+* the LLVM-path reduction loop is unrolled x2 without any ``loop-unroll``
+  pass (the paper's phase-ordered PTX) and each
+  ``loop-unroll`` doubles it (4, 8, then 16); the baseline keeps nvcc's own
+  default (unroll 0 = no pragma);
 * a vectoriser (``bb-vectorize``, ``slp-vectorizer``,
-  ``load-store-vectorizer``, ``loop-vectorize``) running after the loop was
-  unrolled at least x4 forms 128-bit loads;
+  ``load-store-vectorizer``, ``loop-vectorize``) running after a
+  ``loop-unroll`` (so at least 4 adjacent accesses exist) forms 128-bit loads;
 * Blackwell staging: ``loop-interchange`` (needs alias analysis and a
   promoted accumulator) re-maps the loop nest onto warps / smem tiles
   (stage 1); a later ``loop-data-prefetch`` adds the asynchronous staging
@@ -113,7 +115,7 @@ def interpret(order: PhaseOrder) -> VariantState:
         elif n == "loop-unroll":
             unrolls += 1
         elif n in VECTORIZERS:
-            vec = vec or unrolls >= 2
+            vec = vec or unrolls >= 1
         elif n == "loop-interchange":
             interchanged = interchanged or have_aa
         elif n == "loop-data-prefetch":
@@ -122,7 +124,7 @@ def interpret(order: PhaseOrder) -> VariantState:
     stage = 0
     if promoted and interchanged:
         stage = 2 if prefetched else 1
-    unroll = (1, 2, 4)[unrolls] if unrolls < 3 else 8
+    unroll = (2, 4, 8)[unrolls] if unrolls < 3 else 16
     return VariantState(stage=stage, store=store, unroll=unroll, lsr=int(lsr), vec=int(vec))
 
 
