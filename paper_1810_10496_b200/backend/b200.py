@@ -216,6 +216,7 @@ class B200Backend(Backend):
         flush_l2: bool = True,
         min_sample_ms: float = 0.05,
         max_batch: int = 64,
+        slow_ms: float = 50.0,
         memory_budget: float = 100e9,
         types=None,
     ):
@@ -232,6 +233,8 @@ class B200Backend(Backend):
         self.flush_l2 = flush_l2
         self.min_sample_ms = min_sample_ms
         self.max_batch = max_batch
+        self.slow_ms = slow_ms
+        self._first_ms: dict[tuple, float] = {}
         self.memory_budget = memory_budget
         self._ws: "OrderedDict[tuple, Workspace]" = OrderedDict()
         self._artifacts: dict[tuple[str, int], Artifact] = {}
@@ -370,21 +373,26 @@ class B200Backend(Backend):
 
     def _timed(self, ws: Workspace, variant: int) -> list[float]:
         """Median-of-``samples`` device time of one run (ms).  The first use of
-        a (workspace, variant) does an untimed warm-up and sizes the batch so a
-        sample spans at least ``min_sample_ms`` (us-scale kernels)."""
+        a (workspace, variant) does an untimed warm-up (module load, scratch,
+        graph capture) and sizes the batch so a sample spans at least
+        ``min_sample_ms`` (us-scale kernels); runs slower than ``slow_ms`` take
+        a single sample (their relative jitter is already far below 1%)."""
         key = (ws.bench, ws.dims, variant)
         if variant not in ws.warm:
+            ws.run(variant, samples=1, batch=1, restore=True, flush=False)
             first = ws.run(variant, samples=1, batch=1, restore=True, flush=False)[0]
-            self._count(ws.bench, variant, ws.dims, 1)
+            self._count(ws.bench, variant, ws.dims, 2)
             ws.warm.add(variant)
+            self._first_ms[key] = first
             if key not in self._batch:
                 batch = 1
                 if first < self.min_sample_ms:
                     batch = min(self.max_batch, max(1, int(self.min_sample_ms / max(first, 1e-4)) + 1))
                 self._batch[key] = batch
         batch = self._batch.get(key, 1)
-        ms = ws.run(variant, samples=self.samples, batch=batch, restore=True, flush=self.flush_l2)
-        self._count(ws.bench, variant, ws.dims, self.samples * batch)
+        samples = 1 if self._first_ms.get(key, 0.0) > self.slow_ms else self.samples
+        ms = ws.run(variant, samples=samples, batch=batch, restore=True, flush=self.flush_l2)
+        self._count(ws.bench, variant, ws.dims, samples * batch)
         return ms
 
     # ------------------------------------------------------------ conveniences

@@ -204,13 +204,27 @@ __global__ void __launch_bounds__(kFusedThreads, 1) s2_fused(FusedArgs p) {
       dst[c] = q < nq ? __ldcs(a4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
+  // Per-row scalars (column coefficient, row initial value) are fetched one
+  // row ahead together with the row itself: a dependent global load per row
+  // on the critical path costs ~15% of HBM bandwidth otherwise.
+  auto row_scalars = [&](int r, float& coef, float& init) {
+    coef = (do_col && p.colcoef) ? __ldg(p.colcoef + r) : 0.f;
+    init = (t == 0 && p.rowinit) ? p.rowinit[r] : 0.f;
+  };
   int r = blockIdx.x;
-  if (r < p.rows) load_row(r, cur);
+  float coef_cur = 0.f, init_cur = 0.f, coef_nxt = 0.f, init_nxt = 0.f;
+  if (r < p.rows) {
+    load_row(r, cur);
+    row_scalars(r, coef_cur, init_cur);
+  }
   int buf = 0;
   for (; r < p.rows; r += gridDim.x) {
     const int rn = r + gridDim.x;
-    if (rn < p.rows) load_row(rn, nxt);
-    float coef = 0.f;
+    if (rn < p.rows) {
+      load_row(rn, nxt);
+      row_scalars(rn, coef_nxt, init_nxt);
+    }
+    float coef = coef_cur;
     if (do_row) {
       float d = 0.f;
 #pragma unroll
@@ -231,11 +245,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) s2_fused(FusedArgs p) {
 #pragma unroll
       for (int w = 0; w < kFusedThreads / 32; ++w) tot += red[buf][w];
       buf ^= 1;
-      if (t == 0) p.rowout[r] = (p.rowinit ? p.rowinit[r] : 0.f) + tot;
-      coef = tot;
+      if (t == 0) p.rowout[r] = init_cur + tot;
+      if (!p.colcoef) coef = tot;
     }
     if (do_col) {
-      if (p.colcoef) coef = __ldg(p.colcoef + r);
 #pragma unroll
       for (int c = 0; c < C4; ++c) {
         acc[c].x = fmaf(cur[c].x, coef, acc[c].x);
@@ -246,6 +259,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) s2_fused(FusedArgs p) {
     }
 #pragma unroll
     for (int c = 0; c < C4; ++c) cur[c] = nxt[c];
+    coef_cur = coef_nxt;
+    init_cur = init_nxt;
   }
   if (do_col) {
 #pragma unroll

@@ -193,10 +193,10 @@ inline void run(Workspace& ws, cudaStream_t s) {
   }
 }
 
-inline int64_t launches(bool corr, int stage) {
+inline int64_t launches(bool corr, int stage, int64_t m, int64_t n) {
   if (stage == 0) return corr ? 4 : 3;
   const int64_t stats = corr ? 4 : 2;
-  const int64_t gram = stage == 1 ? 1 : tc_gemm_launches(false);
+  const int64_t gram = stage == 1 ? 1 : tc_gemm_launches(m, m, n);
   return stats + 1 + gram + 1 + (corr ? 1 : 0);
 }
 

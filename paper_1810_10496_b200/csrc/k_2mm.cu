@@ -68,7 +68,10 @@ int64_t elems(int a, const Dims& d) {
   const int64_t s[5] = {ni * nk, nk * nj, ni * nj, nj * nl, ni * nl};
   return s[a];
 }
-int64_t launches(int v, const Dims&) { return kTab.v[v].stage == 2 ? 2 * tc_gemm_launches(false) : 2; }
+int64_t launches(int v, const Dims& d) {
+  if (kTab.v[v].stage != 2) return 2;
+  return tc_gemm_launches(d.d[0], d.d[1], d.d[2]) + tc_gemm_launches(d.d[0], d.d[3], d.d[1]);
+}
 double alg_bytes(const Dims& d) {
   const double ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3];
   return 4.0 * (ni * nk + nk * nj + nj * nl + ni * nl);

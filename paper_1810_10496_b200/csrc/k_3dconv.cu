@@ -4,9 +4,9 @@
 // Baseline: the host launches convolution3D_kernel once per plane i
 // (NI-2 launches of a (k, j) grid), 15 global loads per point.  No order
 // helped on the paper's GPU.  Stage 1: one launch, each
-// thread streams along i with the 7 distinct (j, k) taps of a plane kept in a
-// 3-plane register ring (7 loads per output); stage 2: 4 outputs along k per
-// thread with 128-bit loads.
+// thread streams a 16-plane chunk of i with the 7 distinct (j, k) taps of a
+// plane kept in a 3-plane register ring (7 loads per output); stage 2: 4
+// outputs along k per thread with 128-bit loads.
 #include "pf_common.cuh"
 
 #include <algorithm>
@@ -90,6 +90,9 @@ __device__ __forceinline__ Plane7 load_plane(const float* __restrict__ A, size_t
                 __ldg(A + base - nk), __ldg(A + base), __ldg(A + base + nk)};
 }
 
+// planes per CTA in the streaming kernels (i split into chunks for parallelism)
+constexpr int kChunk = 16;
+
 template <BenchId Bn, int V>
 __global__ void __launch_bounds__(256) conv3d_s1(const float* __restrict__ A, float* __restrict__ B, int ni, int nj,
                                                  int nk) {
@@ -98,9 +101,10 @@ __global__ void __launch_bounds__(256) conv3d_s1(const float* __restrict__ A, fl
   if (j <= 0 || j >= nj - 1 || k <= 0 || k >= nk - 1) return;
   const size_t plane = (size_t)nj * nk;
   const size_t col = (size_t)j * nk + k;
-  Plane7 pm = load_plane(A, col, nk);
-  Plane7 pz = load_plane(A, plane + col, nk);
-  for (int i = 1; i < ni - 1; ++i) {
+  const int i0 = 1 + blockIdx.z * kChunk, i1 = min(ni - 1, i0 + kChunk);
+  Plane7 pm = load_plane(A, (size_t)(i0 - 1) * plane + col, nk);
+  Plane7 pz = load_plane(A, (size_t)i0 * plane + col, nk);
+  for (int i = i0; i < i1; ++i) {
     const Plane7 pp = load_plane(A, (size_t)(i + 1) * plane + col, nk);
     Taps t{pm.mm, pm.mp, pm.zp, pm.pp, pz.mz, pz.zz, pz.pz, pp.mm, pp.mp, pp.zp, pp.pp};
     B[(size_t)i * plane + col] = eval15(t);
@@ -134,14 +138,15 @@ __global__ void __launch_bounds__(128) conv3d_s2(const float* __restrict__ A, fl
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   if (j <= 0 || j >= nj - 1 || k0 >= nk) return;
   const size_t plane = (size_t)nj * nk;
+  const int i0 = 1 + blockIdx.z * kChunk, i1 = min(ni - 1, i0 + kChunk);
   // rows (j-1, j, j+1) of planes i-1 and i
   Row6 m[3], z[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    m[d] = load_row6(A, (size_t)(j - 1 + d) * nk, k0, nk);
-    z[d] = load_row6(A, plane + (size_t)(j - 1 + d) * nk, k0, nk);
+    m[d] = load_row6(A, (size_t)(i0 - 1) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
+    z[d] = load_row6(A, (size_t)i0 * plane + (size_t)(j - 1 + d) * nk, k0, nk);
   }
-  for (int i = 1; i < ni - 1; ++i) {
+  for (int i = i0; i < i1; ++i) {
     Row6 p[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) p[d] = load_row6(A, (size_t)(i + 1) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
@@ -180,9 +185,11 @@ struct Run {
       dim3 block(kBX, kBY), grid(cdiv(nk, kBX * (K.vec ? 4 : 1)), cdiv(nj, kBY));
       for (int i = 1; i < ni - 1; ++i) conv3d_s0<B_3DCONV, V><<<grid, block, 0, s>>>(A, B, ni, nj, nk, i);
     } else if constexpr (K.stage == 1) {
-      conv3d_s1<B_3DCONV, V><<<dim3(cdiv(nk, 32), cdiv(nj, 8)), dim3(32, 8), 0, s>>>(A, B, ni, nj, nk);
+      conv3d_s1<B_3DCONV, V><<<dim3(cdiv(nk, 32), cdiv(nj, 8), cdiv(ni - 2, kChunk)), dim3(32, 8), 0, s>>>(A, B, ni, nj,
+                                                                                                    nk);
     } else {
-      conv3d_s2<B_3DCONV, V><<<dim3(cdiv(nk, 4 * 32), cdiv(nj, 4)), dim3(32, 4), 0, s>>>(A, B, ni, nj, nk);
+      conv3d_s2<B_3DCONV, V><<<dim3(cdiv(nk, 4 * 32), cdiv(nj, 4), cdiv(ni - 2, kChunk)), dim3(32, 4), 0, s>>>(
+          A, B, ni, nj, nk);
     }
   }
 };

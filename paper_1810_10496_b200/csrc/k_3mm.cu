@@ -76,7 +76,11 @@ int64_t elems(int a, const Dims& d) {
   const int64_t s[7] = {ni * nk, nk * nj, nj * nm, nm * nl, ni * nj, nj * nl, ni * nl};
   return s[a];
 }
-int64_t launches(int v, const Dims&) { return kTab.v[v].stage == 2 ? 3 * tc_gemm_launches(false) : 3; }
+int64_t launches(int v, const Dims& d) {
+  if (kTab.v[v].stage != 2) return 3;
+  const int64_t ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3], nm = d.d[4];
+  return tc_gemm_launches(ni, nj, nk) + tc_gemm_launches(nj, nl, nm) + tc_gemm_launches(ni, nl, nj);
+}
 double alg_bytes(const Dims& d) {
   const double ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3], nm = d.d[4];
   return 4.0 * (ni * nk + nk * nj + nj * nm + nm * nl + ni * nl);

@@ -41,7 +41,7 @@ int64_t elems(int a, const Dims& d) {
   if (a == 4 - 1) return (m + 1) * (m + 1);
   return m + 1;
 }
-int64_t launches(int v, const Dims&) { return corrcov::launches(true, kTab.v[v].stage); }
+int64_t launches(int v, const Dims& d) { return corrcov::launches(true, kTab.v[v].stage, d.d[0], d.d[1]); }
 double alg_bytes(const Dims& d) {
   const double m = d.d[0], n = d.d[1];
   return 4.0 * ((n + 1) * (m + 1) + (m + 1) * (m + 1));

@@ -121,7 +121,9 @@ int64_t elems(int array, const Dims& d) {
   return array == 0 ? ni * nk : array == 1 ? nk * nj : ni * nj;
 }
 
-int64_t launches(int v, const Dims&) { return kTab.v[v].stage == 2 ? tc_gemm_launches(false) : 1; }
+int64_t launches(int v, const Dims& d) {
+  return kTab.v[v].stage == 2 ? tc_gemm_launches(d.d[0], d.d[1], d.d[2]) : 1;
+}
 
 double alg_bytes(const Dims& d) {
   const double ni = d.d[0], nj = d.d[1], nk = d.d[2];

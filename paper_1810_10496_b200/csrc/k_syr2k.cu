@@ -98,7 +98,9 @@ struct Run {
 constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{});
 
 int64_t elems(int a, const Dims& d) { return a <= 1 ? d.d[0] * d.d[1] : d.d[0] * d.d[0]; }
-int64_t launches(int v, const Dims&) { return kTab.v[v].stage == 2 ? tc_gemm_launches(true) : 1; }
+int64_t launches(int v, const Dims& d) {
+  return kTab.v[v].stage == 2 ? tc_gemm_launches(d.d[0], d.d[0], d.d[1], true) : 1;
+}
 double alg_bytes(const Dims& d) { return 4.0 * (2.0 * d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }
 double alg_flops(const Dims& d) { return 4.0 * (double)d.d[0] * d.d[0] * d.d[1]; }
 int check(int v, const Dims& d) {

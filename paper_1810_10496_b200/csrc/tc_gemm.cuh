@@ -25,6 +25,8 @@
 #pragma once
 #include "pf_common.cuh"
 
+#include <algorithm>
+
 namespace pf {
 
 struct TcGemmArgs {
@@ -54,7 +56,8 @@ struct TcParams {
   const float* alo;
   const float* bhi;
   const float* blo;
-  int kblocks;
+  int kblocks;      // k blocks of the whole reduction
+  int kb_per_split; // k blocks per blockIdx.z (split-K; == kblocks when not split)
   int M, N;
   float alpha, beta;
   const float* Cin;
@@ -237,11 +240,14 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
   tc::fence_after();
   const uint32_t tmem = tmem_slot;
 
-  const size_t a_base = (size_t)mb * p.kblocks * (kTcTile / 4);
-  const size_t b_base = (size_t)nb * p.kblocks * (kTcTile / 4);
+  const int kb0 = blockIdx.z * p.kb_per_split;
+  const int nkb = min(p.kblocks - kb0, p.kb_per_split);
+  const bool split = gridDim.z > 1;
+  const size_t a_base = ((size_t)mb * p.kblocks + kb0) * (kTcTile / 4);
+  const size_t b_base = ((size_t)nb * p.kblocks + kb0) * (kTcTile / 4);
 
   if (warp == 0 && lane == 0) {
-    for (int kb = 0; kb < p.kblocks; ++kb) {
+    for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kTcStages;
       const uint32_t ph = (kb / kTcStages) & 1;
       tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
     }
   } else if (warp == 1 && lane == 0) {
     constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, kTcBN);
-    for (int kb = 0; kb < p.kblocks; ++kb) {
+    for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kTcStages;
       const uint32_t ph = (kb / kTcStages) & 1;
       tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
@@ -291,13 +297,19 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
     if (row < p.M) {
       float* drow = p.D + (size_t)row * p.ldd;
       const float* crow = p.Cin + (size_t)row * p.ldc;
+      if (split) {  // D was pre-scaled by beta; add this k-range's partial
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = col0 + j;
-        if (col < p.N) {
-          float v = p.alpha * __uint_as_float(r[j]);
-          if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
-          drow[col] = v;
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < p.N) atomicAdd(drow + col0 + j, p.alpha * __uint_as_float(r[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = col0 + j;
+          if (col < p.N) {
+            float v = p.alpha * __uint_as_float(r[j]);
+            if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
+            drow[col] = v;
+          }
         }
       }
     }
@@ -309,10 +321,33 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
   }
 }
 
-inline int64_t tc_gemm_launches(bool /*dual*/) { return 3; }  // pack A, pack B, gemm
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Split-K factor: small problems (fewer output tiles than SMs) spread their k
+// blocks over blockIdx.z so that ~148 CTAs run; at least 2 k blocks per split.
+inline int tc_splits(int64_t m, int64_t n, int64_t ktot) {
+  const int64_t tiles = ((m + kTcBM - 1) / kTcBM) * ((n + kTcBN - 1) / kTcBN);
+  const int64_t kblocks = (ktot + kTcBK - 1) / kTcBK;
+  if (tiles >= 74) return 1;
+  int64_t s = std::min<int64_t>(148 / tiles, kblocks / 2);
+  return (int)std::max<int64_t>(1, s);
+}
+
+// pack A, pack B, [pre-scale D when split], gemm
+inline int64_t tc_gemm_launches(int64_t m, int64_t n, int64_t k, bool dual = false) {
+  return 3 + (tc_splits(m, n, dual ? 2 * k : k) > 1 ? 1 : 0);
+}
 inline bool tc_gemm_supported(int64_t m, int64_t n, int64_t k) { return m > 0 && n > 0 && k > 0; }
 
-inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+// D = beta * Cin (or 0) before split-K partials are accumulated atomically.
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) tc_prescale(float* D, int ldd, const float* Cin, int ldc, int M, int N,
+                                                   float beta) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (n >= N) return;
+  D[(size_t)m * ldd + n] = beta != 0.f ? beta * Cin[(size_t)m * ldc + n] : 0.f;
+}
 
 template <BenchId Bn, int V>
 inline void launch_tc_gemm(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
@@ -335,8 +370,12 @@ inline void launch_tc_gemm(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(tc_gemm_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
     configured = true;
   }
-  TcParams p{ahi, alo, bhi, blo, kblocks, a.M, a.N, a.alpha, a.beta, a.Cin, a.ldc, a.D, a.ldd, a.upper_only};
-  tc_gemm_kernel<Bn, V><<<dim3(np / kTcBN, mp / kTcBM), 128, kTcSmem, s>>>(p);
+  const int splits = tc_splits(a.M, a.N, ktot);
+  const int per = (kblocks + splits - 1) / splits;
+  const int zs = (kblocks + per - 1) / per;
+  if (zs > 1) tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
+  TcParams p{ahi, alo, bhi, blo, kblocks, per, a.M, a.N, a.alpha, a.beta, a.Cin, a.ldc, a.D, a.ldd, a.upper_only};
+  tc_gemm_kernel<Bn, V><<<dim3(np / kTcBN, mp / kTcBM, zs), 128, kTcSmem, s>>>(p);
 }
 
 }  // namespace pf

@@ -29,7 +29,7 @@ def main() -> int:
     ap.add_argument("--loo-trials", type=int, default=100)
     ap.add_argument("--benches", nargs="*", default=list(registry.BENCHES))
     ap.add_argument("--out", default="gpurun_out/campaign")
-    ap.add_argument("--samples", type=int, default=1)
+    ap.add_argument("--samples", type=int, default=5)
     args = ap.parse_args()
     be = B200Backend(device=0, samples=args.samples)
     suite = registry.build_suite(be, args.size, benches=args.benches)
