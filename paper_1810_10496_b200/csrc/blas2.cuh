@@ -162,14 +162,19 @@ inline void launch_s1_col_dot(const float* A, int lda, const float* v, int m, in
 }
 
 // ---------------------------------------------------------------- stage 2
-// One pass over A[rows][cols] (cols % 4 == 0).  Thread t owns the float4
-// column chunks q = t + T*c (c < C4).  Per row r:
+// One pass over A[rows][cols] (cols % 4 == 0), persistent CTAs (one per SM).
+// Per row r:
 //   dot_r = sum_j A[r][j] * xv[j]                  (if rowout)
 //   rowout[r] = (rowinit ? rowinit[r] : 0) + dot_r
 //   colacc[j] += A[r][j] * (colcoef ? colcoef[r] : dot_r)   (if colout)
-// xv is staged in shared memory; the next row is prefetched into registers
-// while the current one is reduced; per-CTA column partials are merged with
-// float4 atomics at the end (colout holds its initial value).
+// Rows stream HBM -> shared memory through a kFusedStages-deep ring of
+// cp.async.bulk copies completing on mbarriers (UBLKCP): with 3 x 64 KB in
+// flight per SM the memory pipe stays full without register staging.  Thread
+// t owns the float4 column chunks q = t + T*c (c < C4); xv and the column
+// partials live in its registers; the row dot product is a block reduction
+// (one __syncthreads per row, which also releases the ring slot); per-CTA
+// column partials are merged with float4 atomics at the end (colout holds its
+// initial value).
 struct FusedArgs {
   const float* A;
   int rows, cols;
@@ -181,86 +186,124 @@ struct FusedArgs {
 };
 
 constexpr int kFusedThreads = 512;
+constexpr int kFusedStages = 3;
+
+namespace fused {
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_row(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(0x12F0000000000000ull)  // evict-first policy
+      : "memory");
+}
+}  // namespace fused
 
 template <BenchId Bn, int V, int C4>
 __global__ void __launch_bounds__(kFusedThreads, 1) s2_fused(FusedArgs p) {
-  extern __shared__ float4 xs4[];
+  extern __shared__ __align__(128) float4 ring[];
+  __shared__ __align__(8) uint64_t full[kFusedStages];
   __shared__ float red[2][kFusedThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int nq = p.cols >> 2;
+  const uint32_t row_bytes = (uint32_t)p.cols * 4u;
   const bool do_row = p.rowout != nullptr;
   const bool do_col = p.colout != nullptr;
-  if (do_row)
-    for (int q = t; q < nq; q += kFusedThreads) xs4[q] = __ldg(reinterpret_cast<const float4*>(p.xv) + q);
-  __syncthreads();
-  float4 acc[C4], cur[C4], nxt[C4];
+  // rows of this CTA: r_k = blockIdx.x + k * gridDim.x
+  const int nrows = p.rows > (int)blockIdx.x ? (p.rows - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  if (t == 0) {
+    for (int s = 0; s < kFusedStages; ++s) fused::mbar_init(fused::smem_u32(&full[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < kFusedStages && k < nrows; ++k) {
+      const uint32_t bar = fused::smem_u32(&full[k]);
+      fused::mbar_expect_tx(bar, row_bytes);
+      fused::bulk_row(fused::smem_u32(ring + (size_t)k * nq), p.A + (size_t)(blockIdx.x + k * gridDim.x) * p.cols,
+                      row_bytes, bar);
+    }
+  }
+  float4 xr[C4], acc[C4];
 #pragma unroll
-  for (int c = 0; c < C4; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-  auto load_row = [&](int r, float4 (&dst)[C4]) {
-    const float4* a4 = reinterpret_cast<const float4*>(p.A + (size_t)r * p.cols);
+  for (int c = 0; c < C4; ++c) {
+    const int q = t + kFusedThreads * c;
+    xr[c] = (do_row && q < nq) ? __ldg(reinterpret_cast<const float4*>(p.xv) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  float coef_nxt = 0.f, init_nxt = 0.f;
+  auto scalars = [&](int k) {
+    if (k < nrows) {
+      const int r = blockIdx.x + k * gridDim.x;
+      coef_nxt = (do_col && p.colcoef) ? __ldg(p.colcoef + r) : 0.f;
+      init_nxt = (t == 0 && p.rowinit) ? p.rowinit[r] : 0.f;
+    }
+  };
+  scalars(0);
+  for (int k = 0; k < nrows; ++k) {
+    const int r = blockIdx.x + k * gridDim.x;
+    const int s = k % kFusedStages;
+    float coef = coef_nxt;
+    const float init = init_nxt;
+    scalars(k + 1);
+    fused::mbar_wait(fused::smem_u32(&full[s]), (uint32_t)(k / kFusedStages) & 1u);
+    const float4* row = ring + (size_t)s * nq;
+    float4 v[C4];
 #pragma unroll
     for (int c = 0; c < C4; ++c) {
       const int q = t + kFusedThreads * c;
-      dst[c] = q < nq ? __ldcs(a4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[c] = q < nq ? row[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-  };
-  // Per-row scalars (column coefficient, row initial value) are fetched one
-  // row ahead together with the row itself: a dependent global load per row
-  // on the critical path costs ~15% of HBM bandwidth otherwise.
-  auto row_scalars = [&](int r, float& coef, float& init) {
-    coef = (do_col && p.colcoef) ? __ldg(p.colcoef + r) : 0.f;
-    init = (t == 0 && p.rowinit) ? p.rowinit[r] : 0.f;
-  };
-  int r = blockIdx.x;
-  float coef_cur = 0.f, init_cur = 0.f, coef_nxt = 0.f, init_nxt = 0.f;
-  if (r < p.rows) {
-    load_row(r, cur);
-    row_scalars(r, coef_cur, init_cur);
-  }
-  int buf = 0;
-  for (; r < p.rows; r += gridDim.x) {
-    const int rn = r + gridDim.x;
-    if (rn < p.rows) {
-      load_row(rn, nxt);
-      row_scalars(rn, coef_nxt, init_nxt);
-    }
-    float coef = coef_cur;
+    float tot = 0.f;
     if (do_row) {
       float d = 0.f;
 #pragma unroll
       for (int c = 0; c < C4; ++c) {
-        const int q = t + kFusedThreads * c;
-        if (q < nq) {
-          float4 x = xs4[q];
-          d = fmaf(cur[c].x, x.x, d);
-          d = fmaf(cur[c].y, x.y, d);
-          d = fmaf(cur[c].z, x.z, d);
-          d = fmaf(cur[c].w, x.w, d);
-        }
+        d = fmaf(v[c].x, xr[c].x, d);
+        d = fmaf(v[c].y, xr[c].y, d);
+        d = fmaf(v[c].z, xr[c].z, d);
+        d = fmaf(v[c].w, xr[c].w, d);
       }
       d = warp_sum(d);
-      if (lane == 0) red[buf][warp] = d;
-      __syncthreads();
-      float tot = 0.f;
+      if (lane == 0) red[k & 1][warp] = d;
+    }
+    __syncthreads();  // every thread has read ring slot s (and red is complete)
+    if (t == 0 && k + kFusedStages < nrows) {
+      const uint32_t bar = fused::smem_u32(&full[s]);
+      fused::mbar_expect_tx(bar, row_bytes);
+      fused::bulk_row(fused::smem_u32(ring + (size_t)s * nq),
+                      p.A + (size_t)(blockIdx.x + (k + kFusedStages) * gridDim.x) * p.cols, row_bytes, bar);
+    }
+    if (do_row) {
 #pragma unroll
-      for (int w = 0; w < kFusedThreads / 32; ++w) tot += red[buf][w];
-      buf ^= 1;
-      if (t == 0) p.rowout[r] = init_cur + tot;
+      for (int w = 0; w < kFusedThreads / 32; ++w) tot += red[k & 1][w];
+      if (t == 0) p.rowout[r] = init + tot;
       if (!p.colcoef) coef = tot;
     }
     if (do_col) {
 #pragma unroll
       for (int c = 0; c < C4; ++c) {
-        acc[c].x = fmaf(cur[c].x, coef, acc[c].x);
-        acc[c].y = fmaf(cur[c].y, coef, acc[c].y);
-        acc[c].z = fmaf(cur[c].z, coef, acc[c].z);
-        acc[c].w = fmaf(cur[c].w, coef, acc[c].w);
+        acc[c].x = fmaf(v[c].x, coef, acc[c].x);
+        acc[c].y = fmaf(v[c].y, coef, acc[c].y);
+        acc[c].z = fmaf(v[c].z, coef, acc[c].z);
+        acc[c].w = fmaf(v[c].w, coef, acc[c].w);
       }
     }
-#pragma unroll
-    for (int c = 0; c < C4; ++c) cur[c] = nxt[c];
-    coef_cur = coef_nxt;
-    init_cur = init_nxt;
   }
   if (do_col) {
 #pragma unroll
@@ -277,13 +320,13 @@ inline int fused_c4(int cols) { return (int)cdiv(cols / 4, kFusedThreads); }
 // C4 is one of the instantiated widths.
 inline bool fused_supported(int64_t rows, int64_t cols) {
   if (rows < 1 || cols < 4 || cols % 4) return false;
-  if (cols * 4 > 200 * 1024) return false;
+  if (cols * 4 * kFusedStages > 196 * 1024) return false;
   return fused_c4((int)cols) <= 8;
 }
 
 template <BenchId Bn, int V, int C4>
 inline void launch_fused_c4(const FusedArgs& p, cudaStream_t s) {
-  const size_t smem = (size_t)p.cols * sizeof(float);
+  const size_t smem = (size_t)kFusedStages * p.cols * sizeof(float);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(s2_fused<Bn, V, C4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

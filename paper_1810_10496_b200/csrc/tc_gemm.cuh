@@ -47,9 +47,20 @@ struct TcGemmArgs {
   int upper_only;  // compute only output tiles with n-block >= m-block
 };
 
-constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
-constexpr uint32_t kTcTile = 16384;  // 128 rows x 32 fp32
-constexpr uint32_t kTcSmem = kTcStages * 4 * kTcTile + 1024;
+constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;
+constexpr uint32_t kTcTile = 16384;  // one packed image: 128 rows x 32 fp32
+
+// Tile configurations: BN = 128 (3-stage ring, 64 KB/stage) for small
+// problems, BN = 256 (2-stage ring, 96 KB/stage; N=256 MMAs, 25% less operand
+// traffic per flop) when there are enough output tiles to fill the GPU.
+template <int BN>
+struct TcCfg {
+  static constexpr int kStages = BN == 256 ? 2 : 3;
+  static constexpr uint32_t kBTiles = BN / 128;                       // packed 128-row images per B operand
+  static constexpr uint32_t kStageBytes = (2 + 2 * kBTiles) * kTcTile;  // A hi/lo + B hi/lo
+  static constexpr uint32_t kSmem = kStages * kStageBytes + 1024;
+  static constexpr uint32_t kTmemCols = BN;
+};
 
 struct TcParams {
   const float* ahi;
@@ -211,15 +222,18 @@ __global__ void __launch_bounds__(256) tc_pack(const float* __restrict__ X, cons
   }
 }
 
-template <BenchId Bn, int V>
+template <BenchId Bn, int V, int BN>
 __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
+  using Cfg = TcCfg<BN>;
+  constexpr int kTcStages = Cfg::kStages;
+  constexpr uint32_t kStageBytes = Cfg::kStageBytes;
   extern __shared__ uint8_t tc_smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], accum_bar;
   __shared__ uint32_t tmem_slot;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mb = blockIdx.y, nb = blockIdx.x;
-  if (p.upper_only && nb < mb) return;
+  if (p.upper_only && (nb + 1) * BN <= mb * kTcBM) return;  // tile strictly below the diagonal
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -232,7 +246,7 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_slot)),
-                 "r"(128u));
+                 "r"(Cfg::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc::fence_before();
@@ -244,7 +258,9 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
   const int nkb = min(p.kblocks - kb0, p.kb_per_split);
   const bool split = gridDim.z > 1;
   const size_t a_base = ((size_t)mb * p.kblocks + kb0) * (kTcTile / 4);
-  const size_t b_base = ((size_t)nb * p.kblocks + kb0) * (kTcTile / 4);
+  // B row block nb spans kBTiles packed 128-row images (rb = nb*kBTiles + t)
+  const size_t b_base = ((size_t)nb * Cfg::kBTiles * p.kblocks + kb0) * (kTcTile / 4);
+  const size_t b_tile_stride = (size_t)p.kblocks * (kTcTile / 4);
 
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < nkb; ++kb) {
@@ -252,29 +268,33 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
       const uint32_t ph = (kb / kTcStages) & 1;
       tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
       const uint32_t fb = tc::smem_u32(&full_bar[s]);
-      tc::mbar_expect_tx(fb, 4 * kTcTile);
-      const uint32_t dst = tc::smem_u32(smem + (size_t)s * 4 * kTcTile);
+      tc::mbar_expect_tx(fb, kStageBytes);
+      // stage layout: [A hi][A lo][B hi (kBTiles images)][B lo (kBTiles images)]
+      const uint32_t dst = tc::smem_u32(smem + (size_t)s * kStageBytes);
       const size_t ko = (size_t)kb * (kTcTile / 4);
       tc::bulk_g2s(dst, p.ahi + a_base + ko, kTcTile, fb);
       tc::bulk_g2s(dst + kTcTile, p.alo + a_base + ko, kTcTile, fb);
-      tc::bulk_g2s(dst + 2 * kTcTile, p.bhi + b_base + ko, kTcTile, fb);
-      tc::bulk_g2s(dst + 3 * kTcTile, p.blo + b_base + ko, kTcTile, fb);
+#pragma unroll
+      for (uint32_t t = 0; t < Cfg::kBTiles; ++t) {
+        tc::bulk_g2s(dst + (2 + t) * kTcTile, p.bhi + b_base + t * b_tile_stride + ko, kTcTile, fb);
+        tc::bulk_g2s(dst + (2 + Cfg::kBTiles + t) * kTcTile, p.blo + b_base + t * b_tile_stride + ko, kTcTile, fb);
+      }
     }
   } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, kTcBN);
+    constexpr uint32_t idesc = tc::idesc_tf32(kTcBM, BN);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kTcStages;
       const uint32_t ph = (kb / kTcStages) & 1;
       tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
       tc::fence_after();
-      const uint32_t base = tc::smem_u32(smem + (size_t)s * 4 * kTcTile);
+      const uint32_t base = tc::smem_u32(smem + (size_t)s * kStageBytes);
 #pragma unroll
       for (int kk = 0; kk < kTcBK / 8; ++kk) {
         const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
         const uint64_t ahi = tc::desc_sw128(base + koff);
         const uint64_t alo = tc::desc_sw128(base + kTcTile + koff);
         const uint64_t bhi = tc::desc_sw128(base + 2 * kTcTile + koff);
-        const uint64_t blo = tc::desc_sw128(base + 3 * kTcTile + koff);
+        const uint64_t blo = tc::desc_sw128(base + (2 + Cfg::kBTiles) * kTcTile + koff);
         tc::mma_tf32(tmem, alo, bhi, idesc, (kb | kk) != 0);
         tc::mma_tf32(tmem, ahi, blo, idesc, 1u);
         tc::mma_tf32(tmem, ahi, bhi, idesc, 1u);
@@ -290,10 +310,10 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
   tc::fence_after();
   const int row = mb * kTcBM + warp * 32 + lane;
 #pragma unroll 1
-  for (int c = 0; c < kTcBN / 32; ++c) {
+  for (int c = 0; c < BN / 32; ++c) {
     uint32_t r[32];
     tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32), r);
-    const int col0 = nb * kTcBN + c * 32;
+    const int col0 = nb * BN + c * 32;
     if (row < p.M) {
       float* drow = p.D + (size_t)row * p.ldd;
       const float* crow = p.Cin + (size_t)row * p.ldc;
@@ -317,7 +337,7 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
   tc::fence_before();
   __syncthreads();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
   }
 }
 
@@ -325,8 +345,15 @@ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
 // Split-K factor: small problems (fewer output tiles than SMs) spread their k
 // blocks over blockIdx.z so that ~148 CTAs run; at least 2 k blocks per split.
+inline int tc_bn(int64_t m, int64_t n) {
+  // BN = 256 only when it still yields at least ~one wave of output tiles
+  const int64_t tiles256 = ((m + kTcBM - 1) / kTcBM) * ((n + 255) / 256);
+  return tiles256 >= 120 ? 256 : 128;
+}
+
 inline int tc_splits(int64_t m, int64_t n, int64_t ktot) {
-  const int64_t tiles = ((m + kTcBM - 1) / kTcBM) * ((n + kTcBN - 1) / kTcBN);
+  const int bn = tc_bn(m, n);
+  const int64_t tiles = ((m + kTcBM - 1) / kTcBM) * ((n + bn - 1) / bn);
   const int64_t kblocks = (ktot + kTcBK - 1) / kTcBK;
   if (tiles >= 74) return 1;
   int64_t s = std::min<int64_t>(148 / tiles, kblocks / 2);
@@ -349,10 +376,22 @@ __global__ void __launch_bounds__(256) tc_prescale(float* D, int ldd, const floa
   D[(size_t)m * ldd + n] = beta != 0.f ? beta * Cin[(size_t)m * ldc + n] : 0.f;
 }
 
+template <BenchId Bn, int V, int BN>
+inline void launch_tc_main(const TcParams& p, int np, int mp, int zs, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tc_gemm_kernel<Bn, V, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TcCfg<BN>::kSmem);
+    configured = true;
+  }
+  tc_gemm_kernel<Bn, V, BN><<<dim3(np / BN, mp / kTcBM, zs), 128, TcCfg<BN>::kSmem, s>>>(p);
+}
+
 template <BenchId Bn, int V>
 inline void launch_tc_gemm(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
   const int ktot = a.A2 ? 2 * a.K : a.K;
-  const int mp = round_up(a.M, kTcBM), np = round_up(a.N, kTcBN), kp = round_up(ktot, kTcBK);
+  const int bn = tc_bn(a.M, a.N);
+  const int mp = round_up(a.M, kTcBM), np = round_up(a.N, bn), kp = round_up(ktot, kTcBK);
   const int kblocks = kp / kTcBK;
   const size_t asz = (size_t)mp * kp, bsz = (size_t)np * kp;
   float* scr = ws.ensure_scratch((2 * asz + 2 * bsz) * sizeof(float));
@@ -363,19 +402,17 @@ inline void launch_tc_gemm(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
   float* blo = bhi + bsz;
   tc_pack<Bn, V><<<dim3(kblocks, mp / kTcBM), 256, 0, s>>>(a.A, a.A2, a.lda, a.ta ? 0 : 1, a.M, a.K, ktot, kblocks,
                                                             ahi, alo);
-  tc_pack<Bn, V><<<dim3(kblocks, np / kTcBN), 256, 0, s>>>(a.B, a.B2, a.ldb, a.tb ? 1 : 0, a.N, a.K, ktot, kblocks,
-                                                            bhi, blo);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tc_gemm_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-    configured = true;
-  }
+  tc_pack<Bn, V><<<dim3(kblocks, np / 128), 256, 0, s>>>(a.B, a.B2, a.ldb, a.tb ? 1 : 0, a.N, a.K, ktot, kblocks,
+                                                          bhi, blo);
   const int splits = tc_splits(a.M, a.N, ktot);
   const int per = (kblocks + splits - 1) / splits;
   const int zs = (kblocks + per - 1) / per;
   if (zs > 1) tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
   TcParams p{ahi, alo, bhi, blo, kblocks, per, a.M, a.N, a.alpha, a.beta, a.Cin, a.ldc, a.D, a.ldd, a.upper_only};
-  tc_gemm_kernel<Bn, V><<<dim3(np / kTcBN, mp / kTcBM, zs), 128, kTcSmem, s>>>(p);
+  if (bn == 256)
+    launch_tc_main<Bn, V, 256>(p, np, mp, zs, s);
+  else
+    launch_tc_main<Bn, V, 128>(p, np, mp, zs, s);
 }
 
 }  // namespace pf
