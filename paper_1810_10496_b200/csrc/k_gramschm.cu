@@ -8,7 +8,9 @@
 // from store motion.  Stage 1: block-parallel norm fused
 // with the Q column, the R row as a split-i vector-matrix product, and a
 // 2-D elementwise trailing update; stage 2: the stage-1 sequence captured as
-// one CUDA graph.
+// one CUDA graph (vec=0) or a persistent cooperative kernel with each CTA
+// owning a shared-memory-resident 16-column panel of A and pivot columns
+// handed over through release/acquire flags (vec=1).
 //
 // Input deviation (documented): PolyBench's A = (i+1)(j+1)/(M+1)
 // is rank 1; here A = U[0,1) + N*I so the factorisation is well conditioned.
@@ -19,7 +21,7 @@
 namespace pf {
 namespace {
 
-constexpr auto kTab = make_variants<2, 1, 1, 1>();
+constexpr auto kTab = make_variants<2, 1, 1, 2>();
 constexpr int kNV = sizeof(kTab.v) / sizeof(Knobs);
 
 struct Init {
@@ -171,6 +173,143 @@ void s1_sequence(Workspace& ws, cudaStream_t s) {
   }
 }
 
+// ---- stage 2, vec=1: persistent panel MGS
+// CTA b owns columns [b*W, b*W+W) of A, resident in shared memory (column
+// major, leading dimension m+1 to avoid bank conflicts) for the whole run.
+// Step k: the owner of column k (fully updated by then, since every update of
+// a column is applied by its owner in step order) computes R[k][k] and q_k,
+// writes q_k to a contiguous scratch vector and releases flag[k]; every CTA
+// with columns > k acquires the flag, reads q_k (L2, bypassing L1) and applies
+// the rank-1 update to its columns.  All CTAs must be co-resident: launched
+// cooperatively with grid = ceil(n/W) <= #SMs.
+constexpr int kPanelW = 16;
+constexpr int kPanelThreads = 256;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int W>
+__device__ __forceinline__ void block_sum(float (&v)[W], float (*red)[W], int t) {
+  // warp shuffle, then across the 8 warps through shared memory; result in v (all threads)
+#pragma unroll
+  for (int j = 0; j < W; ++j) v[j] = warp_sum(v[j]);
+  const int warp = t >> 5, lane = t & 31;
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < W; ++j) red[warp][j] = v[j];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < kPanelThreads / 32; ++w) s += red[w][j];
+    v[j] = s;
+  }
+  __syncthreads();
+}
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(kPanelThreads, 1) gs_panel(float* __restrict__ A, float* __restrict__ R,
+                                                             float* __restrict__ Q, float* __restrict__ qbuf,
+                                                             int* __restrict__ flags, int m, int n) {
+  extern __shared__ float S[];  // [W][m + 1]
+  __shared__ float red[kPanelThreads / 32][kPanelW];
+  const int t = threadIdx.x;
+  const int ld = m + 1;
+  const int c0 = blockIdx.x * kPanelW;
+  const int w = min(kPanelW, n - c0);
+  for (int idx = t; idx < m * kPanelW; idx += kPanelThreads) {
+    const int i = idx / kPanelW, jj = idx % kPanelW;
+    if (jj < w) S[jj * ld + i] = A[(size_t)i * n + c0 + jj];
+  }
+  __syncthreads();
+  const int last = c0 + w;  // steps k < last touch this panel
+  for (int k = 0; k < last; ++k) {
+    const bool mine = k >= c0;
+    if (mine) {
+      // pivot column k: norm, R[k][k], q_k
+      const int jj = k - c0;
+      float p[1] = {0.f};
+      for (int i = t; i < m; i += kPanelThreads) p[0] = fmaf(S[jj * ld + i], S[jj * ld + i], p[0]);
+      block_sum<1>(p, reinterpret_cast<float(*)[1]>(red), t);
+      const float rkk = sqrtf(p[0]);
+      if (t == 0) R[(size_t)k * n + k] = rkk;
+      for (int i = t; i < m; i += kPanelThreads) {
+        const float q = S[jj * ld + i] / rkk;
+        qbuf[(size_t)k * m + i] = q;
+        Q[(size_t)i * n + k] = q;
+      }
+      __syncthreads();
+      if (t == 0) {
+        __threadfence();
+        st_release(flags + k, 1);
+      }
+    } else {
+      if (t == 0)
+        while (ld_acquire(flags + k) == 0) {
+        }
+      __syncthreads();
+    }
+    // rank-1 update of this panel's columns j > k with q_k
+    const int j_lo = max(c0, k + 1) - c0;
+    if (j_lo >= w) continue;
+    float r[kPanelW];
+#pragma unroll
+    for (int j = 0; j < kPanelW; ++j) r[j] = 0.f;
+    for (int i = t; i < m; i += kPanelThreads) {
+      const float q = __ldcg(qbuf + (size_t)k * m + i);
+#pragma unroll
+      for (int j = 0; j < kPanelW; ++j)
+        if (j >= j_lo && j < w) r[j] = fmaf(q, S[j * ld + i], r[j]);
+    }
+    block_sum<kPanelW>(r, red, t);
+    if (t < kPanelW && t >= j_lo && t < w) R[(size_t)k * n + c0 + t] = r[t];
+    for (int i = t; i < m; i += kPanelThreads) {
+      const float q = __ldcg(qbuf + (size_t)k * m + i);
+#pragma unroll
+      for (int j = 0; j < kPanelW; ++j)
+        if (j >= j_lo && j < w) S[j * ld + i] = fmaf(-q, r[j], S[j * ld + i]);
+    }
+    __syncthreads();
+  }
+  for (int idx = t; idx < m * kPanelW; idx += kPanelThreads) {
+    const int i = idx / kPanelW, jj = idx % kPanelW;
+    if (jj < w) A[(size_t)i * n + c0 + jj] = S[jj * ld + i];
+  }
+}
+
+inline size_t panel_smem(int m) { return (size_t)kPanelW * (m + 1) * sizeof(float); }
+
+inline bool panel_supported(int64_t m, int64_t n) {
+  return panel_smem((int)m) <= 200 * 1024 && (n + kPanelW - 1) / kPanelW <= 148 && m >= 1 && n >= 1;
+}
+
+template <BenchId Bn, int V>
+void launch_panel(Workspace& ws, cudaStream_t s) {
+  const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
+  float* scratch = ws.ensure_scratch((size_t)n * m * sizeof(float) + (size_t)n * sizeof(int));
+  float* qbuf = scratch;
+  int* flags = reinterpret_cast<int*>(scratch + (size_t)n * m);
+  cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), s);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gs_panel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  float* A = ws.a.p[0];
+  float* R = ws.a.p[1];
+  float* Q = ws.a.p[2];
+  void* args[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n};
+  const int grid = (n + kPanelW - 1) / kPanelW;
+  cudaLaunchCooperativeKernel((const void*)gs_panel<Bn, V>, dim3(grid), dim3(kPanelThreads), args, panel_smem(m), s);
+}
+
 template <int V>
 struct Run {
   static void run(Workspace& ws, cudaStream_t s) {
@@ -187,9 +326,11 @@ struct Run {
       }
     } else if constexpr (K.stage == 1) {
       s1_sequence<B_GRAMSCHM, V>(ws, s);
-    } else {
+    } else if constexpr (K.vec == 0) {
       cudaGraphExec_t g = cached_graph(ws, V, &s1_sequence<B_GRAMSCHM, V>);
       cudaGraphLaunch(g, s);
+    } else {
+      launch_panel<B_GRAMSCHM, V>(ws, s);
     }
   }
 };
@@ -198,8 +339,9 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 
 int64_t elems(int a, const Dims& d) { return a == 1 ? d.d[1] * d.d[1] : d.d[0] * d.d[1]; }
 int64_t launches(int v, const Dims& d) {
-  const int st = kTab.v[v].stage;
-  return st == 0 ? 3 * d.d[1] : 3 * d.d[1] - 2;
+  const Knobs& k = kTab.v[v];
+  if (k.stage == 2 && k.vec) return 1;
+  return k.stage == 0 ? 3 * d.d[1] : 3 * d.d[1] - 2;
 }
 double alg_bytes(const Dims& d) {
   const double m = d.d[0], n = d.d[1];
@@ -207,7 +349,9 @@ double alg_bytes(const Dims& d) {
 }
 double alg_flops(const Dims& d) { return 2.0 * (double)d.d[0] * d.d[1] * d.d[1]; }
 int check(int v, const Dims& d) {
-  if (kTab.v[v].vec && d.d[1] % 4) return 1;
+  const Knobs& k = kTab.v[v];
+  if (k.stage == 0 && k.vec && d.d[1] % 4) return 1;
+  if (k.stage == 2 && k.vec && !panel_supported(d.d[0], d.d[1])) return 1;
   return 0;
 }
 
