@@ -195,14 +195,14 @@ def run_gpu(args, dist: Dist) -> int:
         items += [(ws, c.variant) for c in cands]
 
     for _ in range(max(3, args.warmup)):
-        evaluate_round(items)
+        evaluate_round(items, flush_l2=True)
 
     dist.barrier()
     t_steps = []
     ms_acc = [0.0] * len(items)
     with ClockSampler(device) as clocks:
         for _ in range(args.steps):
-            ms_each, ms_total = evaluate_round(items)
+            ms_each, ms_total = evaluate_round(items, flush_l2=True)
             t_steps.append(ms_total)
             for i, m in enumerate(ms_each):
                 ms_acc[i] += m
@@ -272,11 +272,11 @@ def run_gpu(args, dist: Dist) -> int:
                     hout[a] = ctypes_alloc(lib, nbytes, pinned)
                     d2h += nbytes * len(per_kernel[b]["cands"])
             host_in[ws], host_out[ws] = hin, hout
-        evaluate_round(items, host_in=host_in, host_out=host_out)  # warm
+        evaluate_round(items, flush_l2=True, host_in=host_in, host_out=host_out)  # warm
         dist.barrier()
         e2e_ms = []
         for _ in range(args.e2e_steps):
-            _, tot = evaluate_round(items, host_in=host_in, host_out=host_out)
+            _, tot = evaluate_round(items, flush_l2=True, host_in=host_in, host_out=host_out)
             e2e_ms.append(tot)
         dist.barrier()
         e2e_max = dist.max(sum(e2e_ms) / 1e3)
@@ -300,7 +300,8 @@ def run_gpu(args, dist: Dist) -> int:
             "config": {"workload": f"BLAS-2 set ATAX/BICG/MVT/GESUMMV, N={n} fp32 (BASELINE configs[1])",
                        "n": n, "kernels": list(KERNELS), "orders_per_kernel": args.num_sequences,
                        "evals_per_step_per_gpu": len(items),
-                       "l2": "inputs larger than L2 (A is 1 GiB per kernel); no flush between evaluations",
+                       "l2": "inputs larger than L2 (A is 1-2 GiB per kernel) and L2 flushed (2x L2 memset) "
+                             "before every candidate",
                        "parallelism": f"candidate sharding x{dist.world} (independent streams)"},
             "geomean_speedup": geo,
             "per_kernel": report,

@@ -8,7 +8,7 @@
 #include "pf_common.cuh"
 #include "dense_s0.cuh"
 #include "simt_gemm.cuh"
-#include "tc_gemm.cuh"
+#include "tc_tma.cuh"
 
 namespace pf {
 namespace {
@@ -53,10 +53,10 @@ struct Run {
       launch_simt_gemm<B_2MM, V, false, false, false>(
           SimtGemmArgs{ni, nl, nj, 1.f, 0.f, C, nj, D, nl, nullptr, nullptr, nullptr, nl, E, nl, 0}, s);
     } else {
-      launch_tc_gemm<B_2MM, V>(ws, TcGemmArgs{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr,
-                                              nullptr, nj, C, nj, 0}, s);
-      launch_tc_gemm<B_2MM, V>(ws, TcGemmArgs{ni, nl, nj, 1.f, 0.f, C, nj, false, D, nl, false, nullptr, nullptr,
-                                              nullptr, nl, E, nl, 0}, s);
+      launch_contraction<B_2MM, V>(
+          ws, TcGemmArgs{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr, nullptr, nj, C, nj, 0}, s);
+      launch_contraction<B_2MM, V>(
+          ws, TcGemmArgs{ni, nl, nj, 1.f, 0.f, C, nj, false, D, nl, false, nullptr, nullptr, nullptr, nl, E, nl, 0}, s);
     }
   }
 };
@@ -70,7 +70,8 @@ int64_t elems(int a, const Dims& d) {
 }
 int64_t launches(int v, const Dims& d) {
   if (kTab.v[v].stage != 2) return 2;
-  return tc_gemm_launches(d.d[0], d.d[1], d.d[2]) + tc_gemm_launches(d.d[0], d.d[3], d.d[1]);
+  return tc_launches(d.d[0], d.d[1], d.d[2], tma_ok(d.d[2], d.d[1])) +
+         tc_launches(d.d[0], d.d[3], d.d[1], tma_ok(d.d[1], d.d[3]));
 }
 double alg_bytes(const Dims& d) {
   const double ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3];

@@ -6,7 +6,7 @@
 #include "pf_common.cuh"
 #include "dense_s0.cuh"
 #include "simt_gemm.cuh"
-#include "tc_gemm.cuh"
+#include "tc_tma.cuh"
 
 namespace pf {
 namespace {
@@ -59,11 +59,11 @@ struct Run {
       launch_simt_gemm<B_3MM, V, false, false, false>(
           SimtGemmArgs{ni, nl, nj, 1.f, 0.f, E, nj, F, nl, nullptr, nullptr, nullptr, nl, G, nl, 0}, s);
     } else {
-      launch_tc_gemm<B_3MM, V>(ws, TcGemmArgs{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr,
+      launch_contraction<B_3MM, V>(ws, TcGemmArgs{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr,
                                               nullptr, nj, E, nj, 0}, s);
-      launch_tc_gemm<B_3MM, V>(ws, TcGemmArgs{nj, nl, nm, 1.f, 0.f, C, nm, false, D, nl, false, nullptr, nullptr,
+      launch_contraction<B_3MM, V>(ws, TcGemmArgs{nj, nl, nm, 1.f, 0.f, C, nm, false, D, nl, false, nullptr, nullptr,
                                               nullptr, nl, F, nl, 0}, s);
-      launch_tc_gemm<B_3MM, V>(ws, TcGemmArgs{ni, nl, nj, 1.f, 0.f, E, nj, false, F, nl, false, nullptr, nullptr,
+      launch_contraction<B_3MM, V>(ws, TcGemmArgs{ni, nl, nj, 1.f, 0.f, E, nj, false, F, nl, false, nullptr, nullptr,
                                               nullptr, nl, G, nl, 0}, s);
     }
   }
@@ -79,7 +79,8 @@ int64_t elems(int a, const Dims& d) {
 int64_t launches(int v, const Dims& d) {
   if (kTab.v[v].stage != 2) return 3;
   const int64_t ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3], nm = d.d[4];
-  return tc_gemm_launches(ni, nj, nk) + tc_gemm_launches(nj, nl, nm) + tc_gemm_launches(ni, nl, nj);
+  return tc_launches(ni, nj, nk, tma_ok(nk, nj)) + tc_launches(nj, nl, nm, tma_ok(nm, nl)) +
+         tc_launches(ni, nl, nj, tma_ok(nj, nl));
 }
 double alg_bytes(const Dims& d) {
   const double ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3], nm = d.d[4];

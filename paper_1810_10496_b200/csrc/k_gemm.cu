@@ -9,7 +9,7 @@
 // SIMT kernel; stage 2 the tcgen05 3xTF32 kernel (tc_gemm.cuh).
 #include "pf_common.cuh"
 #include "simt_gemm.cuh"
-#include "tc_gemm.cuh"
+#include "tc_tma.cuh"
 
 namespace pf {
 namespace {
@@ -109,7 +109,7 @@ struct Run {
       launch_simt_gemm<B_GEMM, V, false, false, false>(p, s);
     } else {
       TcGemmArgs p{ni, nj, nk, kAlpha, kBeta, A, nk, false, B, nj, false, nullptr, nullptr, C, nj, C, nj, 0};
-      launch_tc_gemm<B_GEMM, V>(ws, p, s);
+      launch_contraction<B_GEMM, V>(ws, p, s);
     }
   }
 };
@@ -122,7 +122,7 @@ int64_t elems(int array, const Dims& d) {
 }
 
 int64_t launches(int v, const Dims& d) {
-  return kTab.v[v].stage == 2 ? tc_gemm_launches(d.d[0], d.d[1], d.d[2]) : 1;
+  return kTab.v[v].stage == 2 ? tc_launches(d.d[0], d.d[1], d.d[2], tma_ok(d.d[2], d.d[1])) : 1;
 }
 
 double alg_bytes(const Dims& d) {

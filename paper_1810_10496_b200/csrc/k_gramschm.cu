@@ -184,6 +184,7 @@ void s1_sequence(Workspace& ws, cudaStream_t s) {
 // cooperatively with grid = ceil(n/W) <= #SMs.
 constexpr int kPanelW = 16;
 constexpr int kPanelThreads = 256;
+constexpr int kPanelRows = 8;  // rows per thread: m <= 2048
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -229,52 +230,73 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel(float* __restrict__
     if (jj < w) S[jj * ld + i] = A[(size_t)i * n + c0 + jj];
   }
   __syncthreads();
+  // this thread's rows: i_r = t + r * kPanelThreads (r < kPanelRows), valid while < m
+  float q[kPanelRows];
   const int last = c0 + w;  // steps k < last touch this panel
   for (int k = 0; k < last; ++k) {
-    const bool mine = k >= c0;
-    if (mine) {
-      // pivot column k: norm, R[k][k], q_k
+    if (k >= c0) {
+      // pivot column k: fully updated (all its updates were applied here, in order)
       const int jj = k - c0;
       float p[1] = {0.f};
-      for (int i = t; i < m; i += kPanelThreads) p[0] = fmaf(S[jj * ld + i], S[jj * ld + i], p[0]);
+#pragma unroll
+      for (int r = 0; r < kPanelRows; ++r) {
+        const int i = t + r * kPanelThreads;
+        if (i < m) p[0] = fmaf(S[jj * ld + i], S[jj * ld + i], p[0]);
+      }
       block_sum<1>(p, reinterpret_cast<float(*)[1]>(red), t);
       const float rkk = sqrtf(p[0]);
-      if (t == 0) R[(size_t)k * n + k] = rkk;
-      for (int i = t; i < m; i += kPanelThreads) {
-        const float q = S[jj * ld + i] / rkk;
-        qbuf[(size_t)k * m + i] = q;
-        Q[(size_t)i * n + k] = q;
+#pragma unroll
+      for (int r = 0; r < kPanelRows; ++r) {
+        const int i = t + r * kPanelThreads;
+        q[r] = i < m ? S[jj * ld + i] / rkk : 0.f;
+        if (i < m) qbuf[(size_t)k * m + i] = q[r];
       }
       __syncthreads();
       if (t == 0) {
+        R[(size_t)k * n + k] = rkk;
         __threadfence();
         st_release(flags + k, 1);
+      }
+      // Q column store (strided) after the release: off the critical path
+#pragma unroll
+      for (int r = 0; r < kPanelRows; ++r) {
+        const int i = t + r * kPanelThreads;
+        if (i < m) Q[(size_t)i * n + k] = q[r];
       }
     } else {
       if (t == 0)
         while (ld_acquire(flags + k) == 0) {
         }
       __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kPanelRows; ++r) {
+        const int i = t + r * kPanelThreads;
+        q[r] = i < m ? __ldcg(qbuf + (size_t)k * m + i) : 0.f;
+      }
     }
     // rank-1 update of this panel's columns j > k with q_k
     const int j_lo = max(c0, k + 1) - c0;
     if (j_lo >= w) continue;
-    float r[kPanelW];
+    float rj[kPanelW];
 #pragma unroll
-    for (int j = 0; j < kPanelW; ++j) r[j] = 0.f;
-    for (int i = t; i < m; i += kPanelThreads) {
-      const float q = __ldcg(qbuf + (size_t)k * m + i);
+    for (int j = 0; j < kPanelW; ++j) rj[j] = 0.f;
 #pragma unroll
-      for (int j = 0; j < kPanelW; ++j)
-        if (j >= j_lo && j < w) r[j] = fmaf(q, S[j * ld + i], r[j]);
+    for (int r = 0; r < kPanelRows; ++r) {
+      const int i = t + r * kPanelThreads;
+      if (i < m)
+#pragma unroll
+        for (int j = 0; j < kPanelW; ++j)
+          if (j >= j_lo && j < w) rj[j] = fmaf(q[r], S[j * ld + i], rj[j]);
     }
-    block_sum<kPanelW>(r, red, t);
-    if (t < kPanelW && t >= j_lo && t < w) R[(size_t)k * n + c0 + t] = r[t];
-    for (int i = t; i < m; i += kPanelThreads) {
-      const float q = __ldcg(qbuf + (size_t)k * m + i);
+    block_sum<kPanelW>(rj, red, t);
+    if (t < kPanelW && t >= j_lo && t < w) R[(size_t)k * n + c0 + t] = rj[t];
 #pragma unroll
-      for (int j = 0; j < kPanelW; ++j)
-        if (j >= j_lo && j < w) S[j * ld + i] = fmaf(-q, r[j], S[j * ld + i]);
+    for (int r = 0; r < kPanelRows; ++r) {
+      const int i = t + r * kPanelThreads;
+      if (i < m)
+#pragma unroll
+        for (int j = 0; j < kPanelW; ++j)
+          if (j >= j_lo && j < w) S[j * ld + i] = fmaf(-q[r], rj[j], S[j * ld + i]);
     }
     __syncthreads();
   }
@@ -287,7 +309,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel(float* __restrict__
 inline size_t panel_smem(int m) { return (size_t)kPanelW * (m + 1) * sizeof(float); }
 
 inline bool panel_supported(int64_t m, int64_t n) {
-  return panel_smem((int)m) <= 200 * 1024 && (n + kPanelW - 1) / kPanelW <= 148 && m >= 1 && n >= 1;
+  return m <= (int64_t)kPanelThreads * kPanelRows && panel_smem((int)m) <= 200 * 1024 &&
+         (n + kPanelW - 1) / kPanelW <= 148 && m >= 1 && n >= 1;
 }
 
 template <BenchId Bn, int V>

@@ -7,7 +7,7 @@
 // accumulator; stage 2: tcgen05 3xTF32 on the K-concatenation [A B][B A]^T.
 #include "pf_common.cuh"
 #include "simt_gemm.cuh"
-#include "tc_gemm.cuh"
+#include "tc_tma.cuh"
 
 namespace pf {
 namespace {
@@ -89,7 +89,7 @@ struct Run {
       launch_simt_gemm<B_SYR2K, V, false, true, true>(
           SimtGemmArgs{n, n, m, kAlpha, kBeta, A, m, B, m, B, A, C, n, C, n, 0}, s);
     } else {
-      launch_tc_gemm<B_SYR2K, V>(
+      launch_contraction<B_SYR2K, V>(
           ws, TcGemmArgs{n, n, m, kAlpha, kBeta, A, m, false, B, m, true, B, A, C, n, C, n, 0}, s);
     }
   }
@@ -99,7 +99,7 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 
 int64_t elems(int a, const Dims& d) { return a <= 1 ? d.d[0] * d.d[1] : d.d[0] * d.d[0]; }
 int64_t launches(int v, const Dims& d) {
-  return kTab.v[v].stage == 2 ? tc_gemm_launches(d.d[0], d.d[0], d.d[1], true) : 1;
+  return kTab.v[v].stage == 2 ? tc_launches(d.d[0], d.d[0], d.d[1], tma_ok(d.d[1], d.d[1]), true) : 1;
 }
 double alg_bytes(const Dims& d) { return 4.0 * (2.0 * d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }
 double alg_flops(const Dims& d) { return 4.0 * (double)d.d[0] * d.d[0] * d.d[1]; }

@@ -1,0 +1,412 @@
+// Stage-2 contraction kernel, TMA generation: tcgen05 / TMEM 3xTF32 GEMM fed
+// directly from the raw fp32 operands.
+//
+//   D = alpha * op(A) op(B) + beta * Cin        (same contract as tc_gemm.cuh)
+//
+// Differences from the packed path (tc_gemm.cuh):
+//   * no pack kernel and no hi/lo copies in global memory: TMA tensor maps
+//     (cuTensorMapEncodeTiled, SWIZZLE_128B) load the raw fp32 tiles in either
+//     major-ness -- K-major tiles as one 128x32 box, MN-major tiles as four
+//     32x32 boxes -- straight into the canonical UMMA shared-memory layouts;
+//   * the tensor core truncates fp32 to TF32 when it reads an operand, so the
+//     raw tile *is* the "hi" operand (hi = trunc_tf32(x)); four converter warps
+//     compute lo = x - trunc_tf32(x) elementwise into a second buffer (the
+//     operation is layout-agnostic, so one loop serves both major-nesses);
+//   * operand traffic per k block is halved (raw tiles only).
+// Precision: x = hi + lo exactly; the tensor core truncates lo to TF32
+// (|error| <= 2^-10 |lo| <= 2^-20 |x|); the dropped lo*lo term is ~2^-20.
+//
+// Warp roles (192 threads, 1 CTA/SM, 128x128 tile, 3-stage ring of
+// [A raw | B raw | A lo | B lo] = 64 KB):
+//   warp 0 lane 0   TMA producer            full[s]  (expect_tx)
+//   warps 2..5      lo converters           ready[s] (one arrive per warp),
+//                   then the TMEM epilogue (warp w reads TMEM lanes 32*(w%4))
+//   warp 1 lane 0   MMA issuer: 4 k-steps x {lo*hi, hi*lo, hi*hi}; commit -> empty[s]
+//   warp 1          TMEM allocation (128 columns)
+#pragma once
+#include "pf_common.cuh"
+#include "tc_gemm.cuh"
+
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+namespace pf {
+
+constexpr int kTmaStages = 3;
+constexpr uint32_t kTmaTileBytes = 128 * 32 * 4;           // one 128-row x 32-k fp32 tile
+constexpr uint32_t kTmaStageBytes = 4 * kTmaTileBytes;      // A raw, B raw, A lo, B lo
+constexpr uint32_t kTmaSmem = kTmaStages * kTmaStageBytes + 1024;
+constexpr int kTmaThreads = 192;
+
+struct TmaParams {
+  CUtensorMap ta, tb, ta2, tb2;  // 2nd pair: K-concatenated product (SYR2K)
+  int kblocks, kb_per_split, kb1;
+  int a_mn, b_mn;                // operand is MN-major (contiguous along M / N)
+  int M, N;
+  float alpha, beta;
+  const float* Cin;
+  int ldc;
+  float* D;
+  int ldd;
+  int upper_only;
+  uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides / k-step advance (bytes)
+  int idesc_override;                 // probe only: -1 auto, else (a_major | b_major << 1)
+};
+
+namespace tma {
+
+__device__ __forceinline__ void load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// UMMA shared-memory descriptors.
+//   K-major (SWIZZLE_128B, layout 2): 8-row groups of 128-byte rows, SBO 1024 B.
+//   MN-major: for TF32 the only legal MN-major layout is SWIZZLE_128B_BASE32B
+//   (layout 1, Swizzle<2,5,2>: 32-byte chunks of a 128-byte row XORed with
+//   row%4 -- CUTLASS sm100_common.inl); TMA produces it with
+//   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.  128-byte rows hold 32 MN elements of
+//   one K index; 4-row K groups at SBO = 512 B; 32-element MN slabs at
+//   LBO = 4 KB (one 32x32 TMA box each).
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, bool mn_major, uint32_t lbo = 4096u, uint32_t sbo = 512u) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(mn_major ? ((lbo >> 4) & 0x3FFFu) : 1u) << 16;
+  d |= (uint64_t)(((mn_major ? sbo : 1024u) >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)(mn_major ? 1u : 2u) << 61;
+  return d;
+}
+
+__device__ __forceinline__ uint32_t idesc(int m, int n, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+}  // namespace tma
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_constant__ TmaParams p) {
+  extern __shared__ uint8_t tma_smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar;
+  __shared__ uint32_t tmem_slot;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mb = blockIdx.y, nb = blockIdx.x;
+  if (p.upper_only && (nb + 1) * 128 <= mb * 128) return;
+  const int m0 = mb * 128, n0 = nb * 128;
+  const int kb0 = blockIdx.z * p.kb_per_split;
+  const int nkb = min(p.kblocks - kb0, p.kb_per_split);
+  const bool split = gridDim.z > 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      tc::mbar_init(tc::smem_u32(&full_bar[s]), 1);
+      tc::mbar_init(tc::smem_u32(&ready_bar[s]), 4);
+      tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
+    }
+    tc::mbar_init(tc::smem_u32(&accum_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tma::prefetch_map(&p.ta);
+    tma::prefetch_map(&p.tb);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_slot)),
+                 "r"(128u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int kb = kb0 + i;
+        const int s = i % kTmaStages;
+        const uint32_t ph = (i / kTmaStages) & 1;
+        tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
+        const uint32_t fb = tc::smem_u32(&full_bar[s]);
+        tc::mbar_expect_tx(fb, 2 * kTmaTileBytes);
+        const bool second = kb >= p.kb1;
+        const CUtensorMap* ma = second ? &p.ta2 : &p.ta;
+        const CUtensorMap* mbm = second ? &p.tb2 : &p.tb;
+        const int k0 = (second ? kb - p.kb1 : kb) * 32;
+        const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
+        if (p.a_mn) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma::load_2d(base + j * 4096, ma, m0 + 32 * j, k0, fb);
+        } else {
+          tma::load_2d(base, ma, k0, m0, fb);
+        }
+        if (p.b_mn) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma::load_2d(base + kTmaTileBytes + j * 4096, mbm, n0 + 32 * j, k0, fb);
+        } else {
+          tma::load_2d(base + kTmaTileBytes, mbm, k0, n0, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id = p.idesc_override < 0 ? tma::idesc(128, 128, p.a_mn, p.b_mn)
+                                               : tma::idesc(128, 128, p.idesc_override & 1, p.idesc_override >> 1);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kTmaStages;
+        const uint32_t ph = (i / kTmaStages) & 1;
+        tc::mbar_wait(tc::smem_u32(&ready_bar[s]), ph);
+        tc::fence_after();
+        const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t ka = p.a_mn ? kk * p.mn_kstep : kk * 32u;
+          const uint32_t kbo = p.b_mn ? kk * p.mn_kstep : kk * 32u;
+          const uint64_t ahi = tma::desc(base + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
+          const uint64_t bhi = tma::desc(base + kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
+          const uint64_t alo = tma::desc(base + 2 * kTmaTileBytes + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
+          const uint64_t blo = tma::desc(base + 3 * kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
+          tc::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
+          tc::mma_tf32(tmem, ahi, blo, id, 1u);
+          tc::mma_tf32(tmem, ahi, bhi, id, 1u);
+        }
+        tc::mma_commit(tc::smem_u32(&empty_bar[s]));
+      }
+      tc::mma_commit(tc::smem_u32(&accum_bar));
+    }
+    __syncwarp();
+  } else {
+    // ---- converters: lo = x - trunc_tf32(x) for the A and B raw tiles
+    const int ct = threadIdx.x - 64;  // 0..127
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kTmaStages;
+      const uint32_t ph = (i / kTmaStages) & 1;
+      tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
+      const float4* raw = reinterpret_cast<const float4*>(smem + (size_t)s * kTmaStageBytes);
+      float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * kTmaStageBytes + 2 * kTmaTileBytes);
+#pragma unroll 4
+      for (int q = ct; q < (int)(2 * kTmaTileBytes / 16); q += 128) {
+        const float4 v = raw[q];
+        lo[q] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y), v.z - tma::trunc_tf32(v.z),
+                            v.w - tma::trunc_tf32(v.w));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(tc::smem_u32(&ready_bar[s]));
+    }
+    // ---- epilogue: TMEM lanes 32*(warp%4) .. +31 are tile rows
+    tc::mbar_wait(tc::smem_u32(&accum_bar), 0);
+    tc::fence_after();
+    const int quad = warp & 3;
+    const int row = m0 + quad * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32), r);
+      const int col0 = n0 + c * 32;
+      if (row < p.M) {
+        float* drow = p.D + (size_t)row * p.ldd;
+        if (split) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < p.N) atomicAdd(drow + col0 + j, p.alpha * __uint_as_float(r[j]));
+        } else {
+          const float* crow = p.Cin + (size_t)row * p.ldc;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + j;
+            if (col < p.N) {
+              float v = p.alpha * __uint_as_float(r[j]);
+              if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
+              drow[col] = v;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+namespace tma {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeFn encoder() {
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeFn>(f);
+  }();
+  return fn;
+}
+
+// 2-D fp32 tensor map over X[outer][inner] (row pitch ld elements), box
+// {box_inner, box_outer}, out-of-bounds reads as zero.  K-major tiles use
+// SWIZZLE_128B, MN-major tiles SWIZZLE_128B_ATOM_32B (see desc()).
+inline bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, int64_t ld, uint32_t box_inner,
+                     uint32_t box_outer, bool base32) {
+  struct Key {
+    const float* p;
+    int64_t a, b, c;
+    uint32_t d, e;
+    bool f;
+    bool operator==(const Key& o) const {
+      return p == o.p && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e && f == o.f;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      size_t h = std::hash<const void*>()(k.p);
+      for (int64_t v : {k.a, k.b, k.c, (int64_t)k.d, (int64_t)k.e, (int64_t)k.f})
+        h = h * 1000003u ^ std::hash<int64_t>()(v);
+      return h;
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, CUtensorMap, Hash> cache;
+  const Key key{ptr, inner, outer, ld, box_inner, box_outer, base32};
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *map = it->second;
+    return true;
+  }
+  EncodeFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4u};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   base32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *map;
+  return true;
+}
+
+// operand X of logical shape R x K: MN-major (X[k*ld + r]) or K-major (X[r*ld + k])
+inline bool operand_map(CUtensorMap* map, const float* X, bool mn_major, int64_t R, int64_t K, int64_t ld) {
+  if (reinterpret_cast<uintptr_t>(X) % 16 || (ld * 4) % 16) return false;
+  return mn_major ? make_map(map, X, R, K, ld, 32, 32, true) : make_map(map, X, K, R, ld, 32, 128, false);
+}
+
+}  // namespace tma
+
+// True when the TMA path can serve these operands (16-byte aligned bases and
+// pitches); otherwise launch_tc_gemm's packed path is used.
+struct TmaProbe {
+  uint32_t lbo = 4096, sbo = 512, kstep = 1024;
+  int idesc_override = -1;
+};
+inline TmaProbe& tma_probe() {
+  static TmaProbe p;
+  return p;
+}
+
+template <BenchId Bn, int V>
+inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
+  TmaParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.mn_lbo = tma_probe().lbo;
+  p.mn_sbo = tma_probe().sbo;
+  p.mn_kstep = tma_probe().kstep;
+  p.idesc_override = tma_probe().idesc_override;
+  p.a_mn = a.ta ? 1 : 0;
+  p.b_mn = a.tb ? 0 : 1;
+  if (!tma::operand_map(&p.ta, a.A, p.a_mn, a.M, a.K, a.lda)) return false;
+  if (!tma::operand_map(&p.tb, a.B, p.b_mn, a.N, a.K, a.ldb)) return false;
+  if (a.A2) {
+    if (!tma::operand_map(&p.ta2, a.A2, p.a_mn, a.M, a.K, a.lda)) return false;
+    if (!tma::operand_map(&p.tb2, a.B2, p.b_mn, a.N, a.K, a.ldb)) return false;
+  } else {
+    p.ta2 = p.ta;
+    p.tb2 = p.tb;
+  }
+  const int kb1 = (a.K + 31) / 32;
+  const int kblocks = a.A2 ? 2 * kb1 : kb1;
+  const int64_t tiles = (int64_t)((a.M + 127) / 128) * ((a.N + 127) / 128);
+  int splits = 1;
+  if (tiles < 74) splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / tiles, kblocks / 2));
+  const int per = (kblocks + splits - 1) / splits;
+  const int zs = (kblocks + per - 1) / per;
+  if (zs > 1) tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
+  p.kblocks = kblocks;
+  p.kb_per_split = per;
+  p.kb1 = kb1;
+  p.M = a.M;
+  p.N = a.N;
+  p.alpha = a.alpha;
+  p.beta = a.beta;
+  p.Cin = a.Cin;
+  p.ldc = a.ldc;
+  p.D = a.D;
+  p.ldd = a.ldd;
+  p.upper_only = a.upper_only;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tc_tma_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    configured = true;
+  }
+  tc_tma_kernel<Bn, V><<<dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs), kTmaThreads, kTmaSmem, s>>>(p);
+  return true;
+}
+
+// launches of one TMA-path product: [prescale] + gemm
+inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false) {
+  const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  const int64_t kblocks = (dual ? 2 : 1) * ((k + 31) / 32);
+  const bool split = tiles < 74 && std::min<int64_t>(148 / tiles, kblocks / 2) > 1;
+  return split ? 2 : 1;
+}
+
+}  // namespace pf
+
+namespace pf {
+
+// Dims-level predicate matching launch_tc_tma's pointer checks (cudaMalloc
+// bases are 256-byte aligned): pitches and base offsets multiples of 4 floats.
+inline bool tma_ok(int64_t lda, int64_t ldb, int64_t offset_elems = 0) {
+  return lda % 4 == 0 && ldb % 4 == 0 && offset_elems % 4 == 0;
+}
+
+inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual = false) {
+  return tma ? tc_tma_launches(m, n, k, dual) : tc_gemm_launches(m, n, k, dual);
+}
+
+// One tensor-core contraction: TMA-fed raw-operand kernel when possible,
+// otherwise the packed-operand kernel (tc_gemm.cuh).
+template <BenchId Bn, int V>
+inline void launch_contraction(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
+  if (!launch_tc_tma<Bn, V>(a, s)) launch_tc_gemm<Bn, V>(ws, a, s);
+}
+
+}  // namespace pf
