@@ -113,47 +113,45 @@ __global__ void __launch_bounds__(256) conv2d_s1(const float* __restrict__ A, fl
   }
 }
 
-// Stage 2: 4 columns per thread (float4 + 2 halo scalars), kRows rows.
+// Stage 2: 4 columns per thread (float4 + 2 halo scalars), kRows rows; all
+// kRows + 2 input rows are requested before any output is computed so ~30
+// loads per thread are in flight (the kernel is HBM-latency bound otherwise).
 template <BenchId Bn, int V, int kRows>
-__global__ void __launch_bounds__(256) conv2d_s2(const float* __restrict__ A, float* __restrict__ B, int ni, int nj) {
+__global__ void __launch_bounds__(128) conv2d_s2(const float* __restrict__ A, float* __restrict__ B, int ni, int nj) {
   const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   const int i0 = 1 + blockIdx.y * kRows;
   if (j0 >= nj || i0 >= ni - 1) return;
-  float w[3][6];
-  auto load = [&](int d, int rowi) {
-    const float* row = A + (size_t)rowi * nj;
-    const float4 v = __ldg(reinterpret_cast<const float4*>(row + j0));
-    w[d][0] = j0 > 0 ? __ldg(row + j0 - 1) : 0.f;
-    w[d][1] = v.x;
-    w[d][2] = v.y;
-    w[d][3] = v.z;
-    w[d][4] = v.w;
-    w[d][5] = j0 + 4 < nj ? __ldg(row + j0 + 4) : 0.f;
-  };
-  load(0, i0 - 1);
-  load(1, i0);
+  const int rows = min(kRows, ni - 1 - i0);
+  float w[kRows + 2][6];
+#pragma unroll
+  for (int d = 0; d < kRows + 2; ++d) {
+    if (d < rows + 2) {
+      const float* row = A + (size_t)(i0 - 1 + d) * nj;
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(row + j0));
+      w[d][0] = j0 > 0 ? __ldg(row + j0 - 1) : 0.f;
+      w[d][1] = v.x;
+      w[d][2] = v.y;
+      w[d][3] = v.z;
+      w[d][4] = v.w;
+      w[d][5] = j0 + 4 < nj ? __ldg(row + j0 + 4) : 0.f;
+    }
+  }
 #pragma unroll
   for (int r = 0; r < kRows; ++r) {
-    const int i = i0 + r;
-    if (i >= ni - 1) break;
-    load(2, i + 1);
-    float out[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      out[e] = stencil(w[0][e], w[0][e + 1], w[0][e + 2], w[1][e], w[1][e + 1], w[1][e + 2], w[2][e], w[2][e + 1],
-                       w[2][e + 2]);
-    float* brow = B + (size_t)i * nj;
-    if (j0 > 0 && j0 + 4 < nj) {
-      __stcs(reinterpret_cast<float4*>(brow + j0), make_float4(out[0], out[1], out[2], out[3]));
-    } else {
+    if (r < rows) {
+      float out[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (j0 + e > 0 && j0 + e < nj - 1) brow[j0 + e] = out[e];
-    }
+        out[e] = stencil(w[r][e], w[r][e + 1], w[r][e + 2], w[r + 1][e], w[r + 1][e + 1], w[r + 1][e + 2],
+                         w[r + 2][e], w[r + 2][e + 1], w[r + 2][e + 2]);
+      float* brow = B + (size_t)(i0 + r) * nj;
+      if (j0 > 0 && j0 + 4 < nj) {
+        __stcs(reinterpret_cast<float4*>(brow + j0), make_float4(out[0], out[1], out[2], out[3]));
+      } else {
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
-      w[0][c] = w[1][c];
-      w[1][c] = w[2][c];
+        for (int e = 0; e < 4; ++e)
+          if (j0 + e > 0 && j0 + e < nj - 1) brow[j0 + e] = out[e];
+      }
     }
   }
 }
@@ -171,7 +169,7 @@ struct Run {
     } else if constexpr (K.stage == 1) {
       conv2d_s1<B_2DCONV, V, 16><<<dim3(cdiv(nj, 256), cdiv(ni - 2, 16)), 256, 0, s>>>(A, B, ni, nj);
     } else {
-      conv2d_s2<B_2DCONV, V, 16><<<dim3(cdiv(nj, 4 * 128), cdiv(ni - 2, 16)), 128, 0, s>>>(A, B, ni, nj);
+      conv2d_s2<B_2DCONV, V, 8><<<dim3(cdiv(nj, 4 * 128), cdiv(ni - 2, 8)), 128, 0, s>>>(A, B, ni, nj);
     }
   }
 };

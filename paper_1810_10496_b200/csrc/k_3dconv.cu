@@ -146,10 +146,17 @@ __global__ void __launch_bounds__(128) conv3d_s2(const float* __restrict__ A, fl
     m[d] = load_row6(A, (size_t)(i0 - 1) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
     z[d] = load_row6(A, (size_t)i0 * plane + (size_t)(j - 1 + d) * nk, k0, nk);
   }
-  for (int i = i0; i < i1; ++i) {
-    Row6 p[3];
+  // plane i+1 rows are prefetched one iteration ahead (plane i+2 requested
+  // while plane i is computed): two planes of loads in flight per thread
+  Row6 p[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) p[d] = load_row6(A, (size_t)(i + 1) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
+  for (int d = 0; d < 3; ++d) p[d] = load_row6(A, (size_t)(i0 + 1) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
+  for (int i = i0; i < i1; ++i) {
+    Row6 q[3];
+    if (i + 2 < ni) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) q[d] = load_row6(A, (size_t)(i + 2) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
+    }
     float out[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -170,6 +177,7 @@ __global__ void __launch_bounds__(128) conv3d_s2(const float* __restrict__ A, fl
     for (int d = 0; d < 3; ++d) {
       m[d] = z[d];
       z[d] = p[d];
+      p[d] = q[d];
     }
   }
 }

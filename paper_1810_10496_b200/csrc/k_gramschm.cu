@@ -176,15 +176,16 @@ void s1_sequence(Workspace& ws, cudaStream_t s) {
 // ---- stage 2, vec=1: persistent panel MGS
 // CTA b owns columns [b*W, b*W+W) of A, resident in shared memory (column
 // major, leading dimension m+1 to avoid bank conflicts) for the whole run.
-// Step k: the owner of column k (fully updated by then, since every update of
-// a column is applied by its owner in step order) computes R[k][k] and q_k,
-// writes q_k to a contiguous scratch vector and releases flag[k]; every CTA
-// with columns > k acquires the flag, reads q_k (L2, bypassing L1) and applies
-// the rank-1 update to its columns.  All CTAs must be co-resident: launched
-// cooperatively with grid = ceil(n/W) <= #SMs.
+// Inside a CTA, warp w owns panel columns 2w and 2w+1, so every dot product is
+// a warp reduction.  Step k: the warp owning column k (fully updated by then,
+// since all updates of a column are applied by its owner in step order)
+// computes R[k][k] and q_k into shared memory and a contiguous scratch vector
+// and releases flag[k]; every CTA with columns > k acquires the flag, stages
+// q_k (L2, bypassing L1) in shared memory and each warp applies the rank-1
+// update to its columns.  Two block barriers per step.  All CTAs must be
+// co-resident: launched cooperatively with grid = ceil(n/W) <= #SMs.
 constexpr int kPanelW = 16;
 constexpr int kPanelThreads = 256;
-constexpr int kPanelRows = 8;  // rows per thread: m <= 2048
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -195,121 +196,81 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int W>
-__device__ __forceinline__ void block_sum(float (&v)[W], float (*red)[W], int t) {
-  // warp shuffle, then across the 8 warps through shared memory; result in v (all threads)
-#pragma unroll
-  for (int j = 0; j < W; ++j) v[j] = warp_sum(v[j]);
-  const int warp = t >> 5, lane = t & 31;
-  if (lane == 0)
-#pragma unroll
-    for (int j = 0; j < W; ++j) red[warp][j] = v[j];
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < W; ++j) {
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < kPanelThreads / 32; ++w) s += red[w][j];
-    v[j] = s;
-  }
-  __syncthreads();
-}
-
 template <BenchId Bn, int V>
 __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel(float* __restrict__ A, float* __restrict__ R,
                                                              float* __restrict__ Q, float* __restrict__ qbuf,
                                                              int* __restrict__ flags, int m, int n) {
-  extern __shared__ float S[];  // [W][m + 1]
-  __shared__ float red[kPanelThreads / 32][kPanelW];
-  const int t = threadIdx.x;
+  // shared: S [W][m+1] (column-major panel) then qs [m] (q_k of the current step)
+  extern __shared__ float S[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ld = m + 1;
+  float* qs = S + (size_t)kPanelW * ld;
   const int c0 = blockIdx.x * kPanelW;
   const int w = min(kPanelW, n - c0);
   for (int idx = t; idx < m * kPanelW; idx += kPanelThreads) {
     const int i = idx / kPanelW, jj = idx % kPanelW;
     if (jj < w) S[jj * ld + i] = A[(size_t)i * n + c0 + jj];
   }
-  __syncthreads();
-  // this thread's rows: i_r = t + r * kPanelThreads (r < kPanelRows), valid while < m
-  float q[kPanelRows];
-  const int last = c0 + w;  // steps k < last touch this panel
+  // warp `warp` owns panel columns 2*warp and 2*warp+1
+  constexpr int kCols = kPanelW / (kPanelThreads / 32);
+  const int last = c0 + w;
   for (int k = 0; k < last; ++k) {
+    __syncthreads();  // previous step's updates (and reads of qs) are complete
     if (k >= c0) {
-      // pivot column k: fully updated (all its updates were applied here, in order)
       const int jj = k - c0;
-      float p[1] = {0.f};
-#pragma unroll
-      for (int r = 0; r < kPanelRows; ++r) {
-        const int i = t + r * kPanelThreads;
-        if (i < m) p[0] = fmaf(S[jj * ld + i], S[jj * ld + i], p[0]);
-      }
-      block_sum<1>(p, reinterpret_cast<float(*)[1]>(red), t);
-      const float rkk = sqrtf(p[0]);
-#pragma unroll
-      for (int r = 0; r < kPanelRows; ++r) {
-        const int i = t + r * kPanelThreads;
-        q[r] = i < m ? S[jj * ld + i] / rkk : 0.f;
-        if (i < m) qbuf[(size_t)k * m + i] = q[r];
-      }
-      __syncthreads();
-      if (t == 0) {
-        R[(size_t)k * n + k] = rkk;
-        __threadfence();
-        st_release(flags + k, 1);
-      }
-      // Q column store (strided) after the release: off the critical path
-#pragma unroll
-      for (int r = 0; r < kPanelRows; ++r) {
-        const int i = t + r * kPanelThreads;
-        if (i < m) Q[(size_t)i * n + k] = q[r];
+      if (warp == jj / kCols) {
+        const float* col = S + jj * ld;
+        float nrm = 0.f;
+        for (int i = lane; i < m; i += 32) nrm = fmaf(col[i], col[i], nrm);
+        nrm = warp_sum(nrm);
+        const float rkk = sqrtf(nrm);
+        for (int i = lane; i < m; i += 32) {
+          const float q = col[i] / rkk;
+          qs[i] = q;
+          qbuf[(size_t)k * m + i] = q;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          R[(size_t)k * n + k] = rkk;
+          __threadfence();
+          st_release(flags + k, 1);
+        }
       }
     } else {
       if (t == 0)
         while (ld_acquire(flags + k) == 0) {
         }
       __syncthreads();
-#pragma unroll
-      for (int r = 0; r < kPanelRows; ++r) {
-        const int i = t + r * kPanelThreads;
-        q[r] = i < m ? __ldcg(qbuf + (size_t)k * m + i) : 0.f;
-      }
+      for (int i = t; i < m; i += kPanelThreads) qs[i] = __ldcg(qbuf + (size_t)k * m + i);
     }
-    // rank-1 update of this panel's columns j > k with q_k
-    const int j_lo = max(c0, k + 1) - c0;
-    if (j_lo >= w) continue;
-    float rj[kPanelW];
-#pragma unroll
-    for (int j = 0; j < kPanelW; ++j) rj[j] = 0.f;
-#pragma unroll
-    for (int r = 0; r < kPanelRows; ++r) {
-      const int i = t + r * kPanelThreads;
-      if (i < m)
-#pragma unroll
-        for (int j = 0; j < kPanelW; ++j)
-          if (j >= j_lo && j < w) rj[j] = fmaf(q[r], S[j * ld + i], rj[j]);
+    __syncthreads();  // qs holds q_k
+    if (k >= c0 && warp == (k - c0) / kCols) {
+      // the pivot warp also stores the strided Q column (off the other CTAs' critical path)
+      for (int i = lane; i < m; i += 32) Q[(size_t)i * n + k] = qs[i];
     }
-    block_sum<kPanelW>(rj, red, t);
-    if (t < kPanelW && t >= j_lo && t < w) R[(size_t)k * n + c0 + t] = rj[t];
 #pragma unroll
-    for (int r = 0; r < kPanelRows; ++r) {
-      const int i = t + r * kPanelThreads;
-      if (i < m)
-#pragma unroll
-        for (int j = 0; j < kPanelW; ++j)
-          if (j >= j_lo && j < w) S[j * ld + i] = fmaf(-q[r], rj[j], S[j * ld + i]);
+    for (int cc = 0; cc < kCols; ++cc) {
+      const int jj = warp * kCols + cc;
+      if (jj >= w || c0 + jj <= k) continue;
+      float* col = S + jj * ld;
+      float r = 0.f;
+      for (int i = lane; i < m; i += 32) r = fmaf(qs[i], col[i], r);
+      r = warp_sum(r);
+      if (lane == 0) R[(size_t)k * n + c0 + jj] = r;
+      for (int i = lane; i < m; i += 32) col[i] = fmaf(-qs[i], r, col[i]);
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int idx = t; idx < m * kPanelW; idx += kPanelThreads) {
     const int i = idx / kPanelW, jj = idx % kPanelW;
     if (jj < w) A[(size_t)i * n + c0 + jj] = S[jj * ld + i];
   }
 }
 
-inline size_t panel_smem(int m) { return (size_t)kPanelW * (m + 1) * sizeof(float); }
+inline size_t panel_smem(int m) { return ((size_t)kPanelW * (m + 1) + m) * sizeof(float); }
 
 inline bool panel_supported(int64_t m, int64_t n) {
-  return m <= (int64_t)kPanelThreads * kPanelRows && panel_smem((int)m) <= 200 * 1024 &&
+  return panel_smem((int)m) <= 200 * 1024 &&
          (n + kPanelW - 1) / kPanelW <= 148 && m >= 1 && n >= 1;
 }
 
