@@ -187,6 +187,28 @@ def variant_sass(bench: str, variant: int) -> str:
         raise BackendError(f"no SASS recorded for {bench} variant {variant}") from exc
 
 
+def artifact_content(bench: str, variant: int) -> bytes:
+    """The artifact bytes of one variant: a header naming the benchmark and the
+    launch stage, then the normalised SASS.  Variants with identical machine
+    code have identical content, hence identical digests."""
+    knobs = family(bench).knobs[variant]
+    header = f"{ARTIFACT_MAGIC} bench={bench} launch=stage{knobs[0]}\n"
+    return (header + variant_sass(bench, variant)).encode()
+
+
+def variant_of_artifact(bench: str, content: bytes) -> int:
+    """Inverse of ``artifact_content``: the first variant with these bytes."""
+    for v in range(len(family(bench).knobs)):
+        if artifact_content(bench, v) == content:
+            return v
+    raise BackendError(f"artifact is not a {bench} variant of this libpfgpu build")
+
+
+def _supported_dims(bench: str, variant: int, dims) -> bool:
+    rc = _abi.lib().pf_variant_supported(registry.bench_index(bench), variant, _abi.dims_array(dims))
+    return rc == 0
+
+
 def variant_launches(bench: str, variant: int, dims) -> int:
     n = c_int64()
     _abi.check(_abi.lib().pf_variant_launches(registry.bench_index(bench), variant, _abi.dims_array(dims), byref(n)))
@@ -264,9 +286,7 @@ class B200Backend(Backend):
         key = (bench, variant)
         art = self._artifacts.get(key)
         if art is None:
-            knobs = family(bench).knobs[variant]
-            header = f"{ARTIFACT_MAGIC} bench={bench} launch=stage{knobs[0]}\n"
-            art = self.T.Artifact.from_content((header + variant_sass(bench, variant)).encode())
+            art = self.T.Artifact.from_content(artifact_content(bench, variant))
             self._artifacts[key] = art
         return art
 
@@ -307,8 +327,7 @@ class B200Backend(Backend):
         return self.T.ExecutionOutcome(self.T.ExecutionStatus.CRASH, log=str(exc))
 
     def _supported(self, bench: str, variant: int, dims) -> bool:
-        rc = self.lib.pf_variant_supported(registry.bench_index(bench), variant, _abi.dims_array(dims))
-        return rc == 0
+        return _supported_dims(bench, variant, dims)
 
     # ------------------------------------------------------------ Backend API
     def compile(self, kernel: KernelCase, order):
@@ -334,6 +353,13 @@ class B200Backend(Backend):
             raise self.T.BackendError(
                 f"artifact {artifact.digest[:12]} was not compiled from this order for {kernel.id!r}"
             )
+        return self.execute_variant(kernel, bench, variant, input_kind, random_input_index)
+
+    def execute_variant(self, kernel: KernelCase, bench: str, variant: int, input_kind,
+                        random_input_index: int | None = None):
+        """``execute`` after the order -> variant lookup (also the entry of the
+        process-level runner, ``pftool run``)."""
+        artifact = self.artifact(bench, variant)
         try:
             # compare by value: the caller may use the reference's InputKind enum
             if random_input_index is not None or input_kind.value == "validation":

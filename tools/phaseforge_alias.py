@@ -2,9 +2,9 @@
 restated engine, so the reference's own unmodified tests
 (/root/reference/pkg/tests) run against it.
 
-The pure-engine modules (catalog, irfeat, explorer, advisor, results,
-backend.types) come from ``paper_1810_10496_b200``.  The reference's
-simulator, toolchain and CLI sources (out of scope for the B200 build, and
+The engine modules (catalog, irfeat, explorer, advisor, results,
+backend.types, backend.toolchain) come from ``paper_1810_10496_b200``.  The
+reference's simulator and CLI sources (out of scope for the B200 build, and
 used by the reference tests as their test double / front door) are executed
 from /root/reference inside the aliased package, so their relative imports
 bind to the restated types -- a foreign-type mix would fail the engine's
@@ -28,6 +28,7 @@ def _install() -> None:
     if "phaseforge" in sys.modules and getattr(sys.modules["phaseforge"], "__restated__", False):
         return
     from paper_1810_10496_b200 import advisor, catalog, explorer, irfeat, results
+    from paper_1810_10496_b200.backend import toolchain as btoolchain
     from paper_1810_10496_b200.backend import types as btypes
 
     pkg = types.ModuleType("phaseforge")
@@ -52,7 +53,8 @@ def _install() -> None:
         return mod
 
     bpkg.simulator = load("phaseforge.backend.simulator", REF / "backend" / "simulator.py")
-    bpkg.toolchain = load("phaseforge.backend.toolchain", REF / "backend" / "toolchain.py")
+    sys.modules["phaseforge.backend.toolchain"] = btoolchain
+    bpkg.toolchain = btoolchain
     for mod in (btypes, bpkg.simulator, bpkg.toolchain):
         for k in dir(mod):
             if not k.startswith("_"):
