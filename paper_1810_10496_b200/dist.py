@@ -1,5 +1,9 @@
 """One-process-per-GPU plumbing for candidate sharding.
 
+``Dist.map`` is the one scheduling primitive: independent evaluations are
+sharded over ranks and their (small) results gathered to every rank, so all
+ranks hold identical engine state afterwards.
+
 Candidate evaluations are independent, so no collective touches the data
 path: torch.distributed is used only for barriers, the max-over-ranks timing
 reduction, sums of evaluation counts and gathering small result records.
@@ -59,7 +63,45 @@ class Dist:
         self.pg.all_gather_object(out, obj)
         return out
 
+    def map(self, fn, items: list, costs: list[float] | None = None) -> list:
+        """``[fn(x) for x in items]`` with the items sharded over ranks (LPT on
+        ``costs``) and the results gathered to every rank, in item order.  An
+        exception on any rank is re-raised on every rank (after the gather, so
+        no rank is left waiting in it)."""
+        if not self.pg:
+            return [fn(x) for x in items]
+        mine = shard(list(range(len(items))), costs or [1.0] * len(items), self.world, self.rank)
+        local = {}
+        for i in mine:
+            try:
+                local[i] = (True, fn(items[i]))
+            except Exception as exc:  # noqa: BLE001 -- re-raised below on every rank
+                local[i] = (False, exc)
+        merged: dict = {}
+        for part in self.gather(local):
+            merged.update(part)
+        out = []
+        for i in range(len(items)):
+            ok, value = merged[i]
+            if not ok:
+                raise value
+            out.append(value)
+        return out
+
     def close(self) -> None:
         if self.pg:
             self.pg.destroy_process_group()
             self.pg = None
+
+
+def shard(work: list, costs: list[float], world: int, rank: int) -> list:
+    """Longest-processing-time-first assignment; returns this rank's items in
+    their original order."""
+    order = sorted(range(len(work)), key=lambda i: -costs[i])
+    loads = [0.0] * world
+    owner = [0] * len(work)
+    for i in order:
+        r = min(range(world), key=lambda k: loads[k])
+        owner[i] = r
+        loads[r] += costs[i]
+    return [w for i, w in enumerate(work) if owner[i] == rank]

@@ -26,6 +26,7 @@ from dataclasses import dataclass
 from . import _abi, passmodel, registry
 from .backend.b200 import B200Backend, Workspace, family, variant_launches
 from .catalog import PassCatalog, PhaseOrder
+from .dist import shard
 from .explorer import ExplorationConfig, draw_orders
 
 
@@ -98,19 +99,6 @@ def evaluate_round(items: list[tuple[Workspace, int]], restore: bool = True, flu
 
 def launches_of(items: list[tuple[Workspace, int]]) -> int:
     return sum(variant_launches(ws.bench, v, ws.dims) for ws, v in items)
-
-
-def shard(work: list, costs: list[float], world: int, rank: int) -> list:
-    """Longest-processing-time-first assignment; returns this rank's items in
-    their original order."""
-    order = sorted(range(len(work)), key=lambda i: -costs[i])
-    loads = [0.0] * world
-    owner = [0] * len(work)
-    for i in order:
-        r = min(range(world), key=lambda k: loads[k])
-        owner[i] = r
-        loads[r] += costs[i]
-    return [w for i, w in enumerate(work) if owner[i] == rank]
 
 
 __all__ = ["Candidate", "candidate_set", "evaluate_round", "launches_of", "shard"]

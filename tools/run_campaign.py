@@ -1,7 +1,12 @@
 #!/usr/bin/env python3
-"""Run the full 15-benchmark campaign on one GPU (BASELINE configs[4] shape):
+"""Run the full 15-benchmark campaign (BASELINE configs[4] shape):
 explore (num_sequences orders per kernel) -> finalize -> reduce -> KB ->
-speedup report -> leave-one-out 1-NN/3-NN transfer."""
+speedup report -> leave-one-out 1-NN/3-NN transfer.
+
+One GPU: ``python tools/run_campaign.py``.  N GPUs (one process each, the
+evaluations of every step sharded over ranks):
+``python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1
+tools/run_campaign.py``."""
 
 from __future__ import annotations
 
@@ -15,6 +20,7 @@ sys.path.insert(0, str(ROOT))
 from paper_1810_10496_b200 import registry  # noqa: E402
 from paper_1810_10496_b200.backend.b200 import B200Backend  # noqa: E402
 from paper_1810_10496_b200.campaign import run_campaign  # noqa: E402
+from paper_1810_10496_b200.dist import Dist  # noqa: E402
 from paper_1810_10496_b200.explorer import ExplorationConfig  # noqa: E402
 
 
@@ -31,12 +37,18 @@ def main() -> int:
     ap.add_argument("--out", default="gpurun_out/campaign")
     ap.add_argument("--samples", type=int, default=5)
     args = ap.parse_args()
-    be = B200Backend(device=0, samples=args.samples)
+    dist = Dist()
+    be = B200Backend(device=dist.local, samples=args.samples)
     suite = registry.build_suite(be, args.size, benches=args.benches)
     cfg = ExplorationConfig(num_sequences=args.num_sequences, max_len=args.max_len, top_k=args.top_k,
                             final_reps=args.final_reps, final_random_inputs=args.final_random_inputs)
-    res = run_campaign(suite, be, cfg, loo_trials=args.loo_trials, out_dir=args.out)
-    print(f"done in {res.seconds:.0f}s; device runs {be.device_runs}, kernel launches {be.kernel_launches}")
+    log = print if dist.rank == 0 else (lambda *a, **k: None)
+    res = run_campaign(suite, be, cfg, loo_trials=args.loo_trials, out_dir=args.out, dist=dist, log=log)
+    runs = dist.sum(be.device_runs)
+    launches = dist.sum(be.kernel_launches)
+    seconds = dist.max(res.seconds)
+    log(f"done in {seconds:.0f}s on {dist.world} GPU(s); device runs {runs:.0f}, kernel launches {launches:.0f}")
+    dist.close()
     return 0
 
 
