@@ -20,6 +20,7 @@ model and whose inputs are opaque strings.  Here:
 from __future__ import annotations
 
 from dataclasses import dataclass
+from pathlib import Path
 
 from .backend.types import KernelCase
 
@@ -234,9 +235,27 @@ def _ir_texts() -> dict[str, str]:
 
 IR_TEXTS = _ir_texts()
 
+# The second feature source: IR-subset text recovered from the -O0 PTX of each
+# benchmark's compiled baseline variant (tools/gen_ir.py, committed under ir/).
+IR_DIR = Path(__file__).resolve().parent / "ir"
+IR_SOURCES = ("structural", "ptx")
+
+
+def ir_text(bench: str, source: str = "structural") -> str:
+    """``structural``: the PolyBench/GPU kernel shapes above (the default, used
+    by the golden fixtures); ``ptx``: generated from the baseline variant's PTX."""
+    if source == "structural":
+        return IR_TEXTS[bench]
+    if source == "ptx":
+        path = IR_DIR / f"{bench}.ir"
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing: run tools/gen_ir.py")
+        return path.read_text()
+    raise ValueError(f"unknown IR source {source!r} (expected one of {IR_SOURCES})")
+
 
 def kernel_case(bench: str, size: str = "config", reference_outputs: tuple[float, ...] = (),
-                validation_dims=None, measurement_dims=None) -> KernelCase:
+                validation_dims=None, measurement_dims=None, ir: str = "structural") -> KernelCase:
     """A ``KernelCase`` for ``bench``; reference outputs are filled by ``build_suite``."""
     sizes = SIZES[bench]
     vdims = validation_dims or sizes["validation"]
@@ -247,16 +266,16 @@ def kernel_case(bench: str, size: str = "config", reference_outputs: tuple[float
         validation_input=describe(bench, vdims),
         measurement_input=describe(bench, mdims),
         reference_outputs=tuple(reference_outputs),
-        ir_text=IR_TEXTS[bench],
+        ir_text=ir_text(bench, ir),
     )
 
 
-def build_suite(backend, size: str = "config", benches=BENCHES, **dims_override) -> list[KernelCase]:
+def build_suite(backend, size: str = "config", benches=BENCHES, ir: str = "structural") -> list[KernelCase]:
     """KernelCases with ``reference_outputs`` = baseline-variant outputs on the
     validation input, computed on the device through ``backend``."""
     cases = []
     for b in benches:
-        case = kernel_case(b, size)
+        case = kernel_case(b, size, ir=ir)
         outs = backend.baseline_outputs(case)
         cases.append(KernelCase(case.id, case.source, case.validation_input, case.measurement_input,
                                 tuple(outs), case.ir_text))
@@ -275,6 +294,7 @@ __all__ = [
     "bench_of",
     "build_suite",
     "describe",
+    "ir_text",
     "kernel_case",
     "parse_descriptor",
     "source_of",

@@ -36,10 +36,12 @@ def main() -> int:
     ap.add_argument("--benches", nargs="*", default=list(registry.BENCHES))
     ap.add_argument("--out", default="gpurun_out/campaign")
     ap.add_argument("--samples", type=int, default=5)
+    ap.add_argument("--ir", default="structural", choices=registry.IR_SOURCES,
+                    help="feature source: PolyBench-shaped IR (default) or IR recovered from the baseline PTX")
     args = ap.parse_args()
     dist = Dist()
     be = B200Backend(device=dist.local, samples=args.samples)
-    suite = registry.build_suite(be, args.size, benches=args.benches)
+    suite = registry.build_suite(be, args.size, benches=args.benches, ir=args.ir)
     cfg = ExplorationConfig(num_sequences=args.num_sequences, max_len=args.max_len, top_k=args.top_k,
                             final_reps=args.final_reps, final_random_inputs=args.final_random_inputs)
     log = print if dist.rank == 0 else (lambda *a, **k: None)
