@@ -29,6 +29,7 @@
 
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -247,6 +248,230 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair kernel
+// Same contract and per-CTA stage layout as tc_tma_kernel, but two CTAs of a
+// cluster (one TPC) cooperate on a 256x256 tile with tcgen05.mma.cta_group::2
+// (M = 256, N = 256): CTA r holds A rows m0 + 128r .. +127 and B columns
+// n0 + 128r .. +127 of every k block, and accumulates its 128 rows x all 256
+// columns in its own TMEM.  Each CTA streams half of the B tile the pair needs,
+// so shared-memory operand traffic per FMA halves -- the single-CTA kernel is
+// shared-memory-bandwidth bound (ncu, profiles/r01_ncu_tc_tma.md).
+//   * each CTA: TMA producer (own full[s]) -> 4 converter warps (lo) -> one
+//     arrive per warp on the LEADER's ready[s] (8 arrivals per phase);
+//   * leader warp 1 lane 0 issues the MMAs; tcgen05.commit multicasts to
+//     empty[s] / accum in both CTAs;
+//   * TMEM: 256 columns allocated with cta_group::2 by warp 1 of both CTAs.
+// Every wait is bounded (~10 s of clock64) and traps instead of hanging.
+namespace tc2 {
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t peer_addr(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ bool try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void wait(uint32_t bar, uint32_t parity) {
+  if (try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  for (uint32_t n = 1;; ++n) {
+    if (try_wait(bar, parity)) return;
+    if ((n & 1023u) == 0 && clock64() - t0 > 20000000000LL) __trap();
+  }
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void commit_both(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+}  // namespace tc2
+
+template <BenchId Bn, int V>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
+    tc_tma2_kernel(const __grid_constant__ TmaParams p) {
+  extern __shared__ uint8_t tma_smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar;
+  __shared__ uint32_t tmem_slot;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc2::cluster_rank();
+  const int mb = blockIdx.y, nb = blockIdx.x >> 1;
+  if (p.upper_only && nb < mb) return;  // the whole pair leaves together
+  const int m0 = mb * 256 + (int)rank * 128;  // A rows / accumulator rows of this CTA
+  const int nB = nb * 256 + (int)rank * 128;  // B columns streamed by this CTA
+  const int n0 = nb * 256;                    // accumulator columns (both CTAs)
+  const int kb0 = blockIdx.z * p.kb_per_split;
+  const int nkb = min(p.kblocks - kb0, p.kb_per_split);
+  const bool split = gridDim.z > 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      tc::mbar_init(tc::smem_u32(&full_bar[s]), 1);
+      tc::mbar_init(tc::smem_u32(&ready_bar[s]), 8);
+      tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
+    }
+    tc::mbar_init(tc::smem_u32(&accum_bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tma::prefetch_map(&p.ta);
+    tma::prefetch_map(&p.tb);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tmem_slot)),
+                 "r"(256u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc::fence_before();
+  tc2::cluster_sync();
+  tc::fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int kb = kb0 + i;
+        const int s = i % kTmaStages;
+        const uint32_t ph = (i / kTmaStages) & 1;
+        tc2::wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
+        const uint32_t fb = tc::smem_u32(&full_bar[s]);
+        tc::mbar_expect_tx(fb, 2 * kTmaTileBytes);
+        const bool second = kb >= p.kb1;
+        const CUtensorMap* ma = second ? &p.ta2 : &p.ta;
+        const CUtensorMap* mbm = second ? &p.tb2 : &p.tb;
+        const int k0 = (second ? kb - p.kb1 : kb) * 32;
+        const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
+        if (p.a_mn) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma::load_2d(base + j * 4096, ma, m0 + 32 * j, k0, fb);
+        } else {
+          tma::load_2d(base, ma, k0, m0, fb);
+        }
+        if (p.b_mn) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma::load_2d(base + kTmaTileBytes + j * 4096, mbm, nB + 32 * j, k0, fb);
+        } else {
+          tma::load_2d(base + kTmaTileBytes, mbm, k0, nB, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t id = tma::idesc(256, 256, p.a_mn, p.b_mn);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kTmaStages;
+        const uint32_t ph = (i / kTmaStages) & 1;
+        tc2::wait(tc::smem_u32(&ready_bar[s]), ph);
+        tc::fence_after();
+        const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t ka = p.a_mn ? kk * p.mn_kstep : kk * 32u;
+          const uint32_t kbo = p.b_mn ? kk * p.mn_kstep : kk * 32u;
+          const uint64_t ahi = tma::desc(base + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
+          const uint64_t bhi = tma::desc(base + kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
+          const uint64_t alo = tma::desc(base + 2 * kTmaTileBytes + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
+          const uint64_t blo = tma::desc(base + 3 * kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
+          tc2::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
+          tc2::mma_tf32(tmem, ahi, blo, id, 1u);
+          tc2::mma_tf32(tmem, ahi, bhi, id, 1u);
+        }
+        tc2::commit_both(tc::smem_u32(&empty_bar[s]));
+      }
+      tc2::commit_both(tc::smem_u32(&accum_bar));
+    }
+    __syncwarp();
+  } else {
+    const int ct = threadIdx.x - 64;  // 0..127
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kTmaStages;
+      const uint32_t ph = (i / kTmaStages) & 1;
+      tc2::wait(tc::smem_u32(&full_bar[s]), ph);
+      const float4* raw = reinterpret_cast<const float4*>(smem + (size_t)s * kTmaStageBytes);
+      float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * kTmaStageBytes + 2 * kTmaTileBytes);
+#pragma unroll 4
+      for (int q = ct; q < (int)(2 * kTmaTileBytes / 16); q += 128) {
+        const float4 v = raw[q];
+        lo[q] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y), v.z - tma::trunc_tf32(v.z),
+                            v.w - tma::trunc_tf32(v.w));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tc2::arrive_remote(tc2::peer_addr(tc::smem_u32(&ready_bar[s]), 0));
+    }
+    tc2::wait(tc::smem_u32(&accum_bar), 0);
+    tc::fence_after();
+    const int quad = warp & 3;
+    const int row = m0 + quad * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32), r);
+      const int col0 = n0 + c * 32;
+      if (row < p.M) {
+        float* drow = p.D + (size_t)row * p.ldd;
+        if (split) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < p.N) atomicAdd(drow + col0 + j, p.alpha * __uint_as_float(r[j]));
+        } else {
+          const float* crow = p.Cin + (size_t)row * p.ldc;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = col0 + j;
+            if (col < p.N) {
+              float v = p.alpha * __uint_as_float(r[j]);
+              if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
+              drow[col] = v;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  tc2::cluster_sync();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u));
+  }
+}
+
 // ---------------------------------------------------------------- host side
 namespace tma {
 
@@ -332,6 +557,25 @@ inline TmaProbe& tma_probe() {
   return p;
 }
 
+// CTA-pair (256x256) tiles for products with at least one full pair tile;
+// PF_TC_PAIR=0 in the environment forces the single-CTA kernel (A/B runs).
+inline bool tc_pair_ok(int64_t m, int64_t n) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("PF_TC_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return enabled && m >= 256 && n >= 256;
+}
+
+// split-K factor: fill ~148 SMs when the output has too few tiles
+inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair) {
+  const int64_t ctas = pair ? 2 * ((m + 255) / 256) * ((n + 255) / 256) : ((m + 127) / 128) * ((n + 127) / 128);
+  int splits = 1;
+  if (ctas < 74) splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / ctas, kblocks / 2));
+  const int per = (kblocks + splits - 1) / splits;
+  return (kblocks + per - 1) / per;
+}
+
 template <BenchId Bn, int V>
 inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
   TmaParams p;
@@ -353,11 +597,9 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
   }
   const int kb1 = (a.K + 31) / 32;
   const int kblocks = a.A2 ? 2 * kb1 : kb1;
-  const int64_t tiles = (int64_t)((a.M + 127) / 128) * ((a.N + 127) / 128);
-  int splits = 1;
-  if (tiles < 74) splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / tiles, kblocks / 2));
-  const int per = (kblocks + splits - 1) / splits;
-  const int zs = (kblocks + per - 1) / per;
+  const bool pair = tc_pair_ok(a.M, a.N);
+  const int zs = tc_tma_splits(a.M, a.N, kblocks, pair);
+  const int per = (kblocks + zs - 1) / zs;
   if (zs > 1) tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
   p.kblocks = kblocks;
   p.kb_per_split = per;
@@ -374,18 +616,20 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tc_tma_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    cudaFuncSetAttribute(tc_tma2_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     configured = true;
   }
-  tc_tma_kernel<Bn, V><<<dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs), kTmaThreads, kTmaSmem, s>>>(p);
+  if (pair)
+    tc_tma2_kernel<Bn, V><<<dim3(2 * cdiv(a.N, 256), cdiv(a.M, 256), zs), kTmaThreads, kTmaSmem, s>>>(p);
+  else
+    tc_tma_kernel<Bn, V><<<dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs), kTmaThreads, kTmaSmem, s>>>(p);
   return true;
 }
 
 // launches of one TMA-path product: [prescale] + gemm
 inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false) {
-  const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
-  const int64_t kblocks = (dual ? 2 : 1) * ((k + 31) / 32);
-  const bool split = tiles < 74 && std::min<int64_t>(148 / tiles, kblocks / 2) > 1;
-  return split ? 2 : 1;
+  const int kblocks = (int)((dual ? 2 : 1) * ((k + 31) / 32));
+  return tc_tma_splits(m, n, kblocks, tc_pair_ok(m, n)) > 1 ? 2 : 1;
 }
 
 }  // namespace pf

@@ -163,6 +163,14 @@ def _classify(opcode: str, operands: str, addr_adds: set, folded: set) -> list[s
 
 def translate(name: str, lines: list[str]) -> str:
     stmts = list(_statements(lines))
+    # PTX labels carry a module-wide function counter ($L__BB<fn>_<n>); rename
+    # them in order of definition so the text depends on this function only
+    rename = {}
+    for kind, s in stmts:
+        if kind == "label":
+            rename[s] = f"bb{len(rename) + 1}"
+    stmts = [(k, rename[s] if k == "label" else re.sub(r"\$?L__BB\w+", lambda m: rename.get(m.group(0), m.group(0)), s))
+             for k, s in stmts]
     # address recognition: 64-bit adds whose result is a memory operand, and
     # the shift / wide-multiply / index-extension feeding only them
     mem_regs = {m.group(1) for kind, s in stmts if kind == "insn" for m in _ADDR_OPND.finditer(s)}
