@@ -246,7 +246,7 @@ def run_gpu(args, dist: Dist) -> int:
         bytes_, _ = alg_work(b, ws.dims)
         achieved = bytes_ / (ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": args.traffic,
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": args.traffic or ncu_traffic(b, items[i][1]),
                     "kernel": f"{b} {family(b).key(items[i][1])}",
                     "alg_bytes_per_launch": bytes_, "mean_launch_ms": ms,
                     "peak_source": peaks["source"] + " (burst copy, MEASURED_PEAKS.json)"}
@@ -314,6 +314,19 @@ def run_gpu(args, dist: Dist) -> int:
         print(json.dumps(line), flush=True)
     be.close()
     return 0
+
+
+def ncu_traffic(bench: str, variant: int):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu
+    --set full capture (profiles/r01_traffic.json), or None."""
+    from paper_1810_10496_b200.backend.b200 import family
+
+    path = ROOT / "profiles" / "r01_traffic.json"
+    try:
+        entry = json.loads(path.read_text()).get(f"{bench} {family(bench).key(variant)}")
+    except (OSError, ValueError):
+        return None
+    return entry["traffic"] if entry else None
 
 
 def ctypes_alloc(lib, nbytes: int, keep: list):

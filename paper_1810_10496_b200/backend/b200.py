@@ -90,6 +90,10 @@ class Workspace:
         _abi.check(self.lib.pf_run_e2e(self.handle, variant, samples, hin, hout, ms))
         return list(ms)
 
+    def restore(self) -> None:
+        """Reset in-place (INOUT) arrays to the generated input (pf_ws_restore)."""
+        _abi.check(self.lib.pf_ws_restore(self.handle))
+
     def download(self, array: int):
         import numpy as np
 

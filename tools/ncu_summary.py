@@ -90,6 +90,13 @@ def main() -> int:
             for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))[:25]:
                 lines.append(f"| `{name[:90]}` | {len(v)} | {sum(v):.0f} | {100 * sum(v) / total:.1f}% |")
             lines.append("")
+            profiled = {d.get("Kernel Name", "?") for rep in sorted(src.glob("*.ncu-rep")) for d in raw(rep)}
+            lines += ["Share of the step for the kernels captured above (cold-cache, serialised):", ""]
+            for name in sorted(profiled):
+                v = agg.get(name, [])
+                lines.append(f"* `{name[:90]}`: {len(v)} launches, {sum(v):.0f} ns, {100 * sum(v) / total:.2f}% "
+                             f"of the step, mean {sum(v) / max(1, len(v)):.0f} ns/launch")
+            lines.append("")
     dst.write_text("\n".join(lines) + "\n")
     print(f"wrote {dst}")
     return 0
