@@ -109,8 +109,9 @@ int pf_ws_array_ptr(pf_ws* ws, int array, void** dptr);
  * One sample = [restore] -> [L2 flush] -> event0 -> `batch` x variant run ->
  * event1.  ms[s] = elapsed / batch.  restore!=0 restores in-place state before
  * every sample (outputs of the last sample are then those of one run when
- * batch==1).  flush_l2!=0 writes a scratch buffer of 2 x L2 before each
- * sample.  Synchronises the workspace stream. */
+ * batch==1).  flush_l2!=0 writes a scratch buffer of 2 x L2 and reads it
+ * back before each sample (L2 left clean: no write-backs inside the timed
+ * run).  Synchronises the workspace stream. */
 int pf_run(pf_ws* ws, int variant, int samples, int batch, int restore, int flush_l2, float* ms);
 /* End-to-end: per sample, H2D of every generated input array from `host_in`
  * (array-indexed table of host pointers, NULL entries skipped), restore of

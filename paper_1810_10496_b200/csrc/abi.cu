@@ -47,6 +47,17 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
+// Streams the flush buffer through L2 (loads only; the store never happens
+// for the 0x5a fill pattern, it only keeps the loads alive).
+__global__ void __launch_bounds__(512) flush_read_kernel(const float4* __restrict__ p, int64_t n4, float* sink) {
+  float acc = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = p[i];
+    acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 1.2345f) sink[0] = acc;
+}
+
 // Per-device L2 flush buffer (2 x L2), grown lazily under a lock.
 struct FlushBuf {
   void* ptr = nullptr;
@@ -68,7 +79,15 @@ int flush_l2(int device, cudaStream_t s) {
       fb->bytes = want;
     }
   }
+  // Write the buffer (evicts everything), then read it back: the read sweep
+  // writes the memset's dirty lines back to HBM here, outside the timed
+  // region, so the next kernel starts on a clean L2 instead of paying up to
+  // one L2 of write-backs inside its own measurement.
   PF_CUDA(cudaMemsetAsync(fb->ptr, 0x5a, fb->bytes, s));
+  const int64_t n4 = (int64_t)(fb->bytes / sizeof(float4));
+  flush_read_kernel<<<4 * 148, 512, 0, s>>>(reinterpret_cast<const float4*>(fb->ptr), n4,
+                                            reinterpret_cast<float*>(fb->ptr));
+  PF_CUDA(cudaGetLastError());
   return PF_OK;
 }
 
@@ -394,6 +413,7 @@ int pf_ws_generate(pf_ws* ws, int stock, uint64_t seed, int64_t instance) {
     }
   }
   PF_CUDA(cudaGetLastError());
+  if (const char* why = take_launch_error()) return fail(PF_ECUDA, why);
   if (int rc = snapshot(ws)) return rc;
   PF_CUDA(cudaStreamSynchronize(ws->stream));
   return PF_OK;
@@ -460,6 +480,7 @@ int pf_run(pf_ws* ws, int variant, int samples, int batch, int restore, int flus
     PF_CUDA(cudaEventRecord(ws->ev0, ws->stream));
     for (int b = 0; b < batch; ++b) fn(*ws, ws->stream);
     PF_CUDA(cudaGetLastError());
+    if (const char* why = take_launch_error()) return fail(PF_ECUDA, why);
     PF_CUDA(cudaEventRecord(ws->ev1, ws->stream));
     PF_CUDA(cudaEventSynchronize(ws->ev1));
     float t = 0.f;
@@ -487,6 +508,7 @@ int pf_run_e2e(pf_ws* ws, int variant, int samples, float* const* host_in, float
     }
     fn(*ws, ws->stream);
     PF_CUDA(cudaGetLastError());
+    if (const char* why = take_launch_error()) return fail(PF_ECUDA, why);
     for (int a = 0; a < d->narrays; ++a)
       if (d->arrays[a].is_output && host_out && host_out[a])
         PF_CUDA(cudaMemcpyAsync(host_out[a], ws->a.p[a], ws->elems[a] * sizeof(float), cudaMemcpyDeviceToHost,
@@ -549,6 +571,7 @@ int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush, float* ms
     PF_CUDA(cudaEventRecord(pool[2 * i], st));
     d->run[evals[i].variant](*ws, st);
     PF_CUDA(cudaGetLastError());
+    if (const char* why = take_launch_error()) return fail(PF_ECUDA, why);
     PF_CUDA(cudaEventRecord(pool[2 * i + 1], st));
     if (evals[i].host_out) {
       for (int a = 0; a < d->narrays; ++a)

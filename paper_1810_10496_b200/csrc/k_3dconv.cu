@@ -8,6 +8,8 @@
 // plane kept in a 3-plane register ring (7 loads per output); stage 2: 4
 // outputs along k per thread with 128-bit loads.
 #include "pf_common.cuh"
+#include "tc_gemm.cuh"
+#include "tma_map.cuh"
 
 #include <algorithm>
 
@@ -113,73 +115,160 @@ __global__ void __launch_bounds__(256) conv3d_s1(const float* __restrict__ A, fl
   }
 }
 
-// 4 consecutive k per thread: per plane row offset dj, a float4 at k0 plus the
-// k0-1 and k0+4 halo scalars.
-struct Row6 {
-  float v[6];  // k0-1 .. k0+4
+// Stage 2: TMA-fed plane streaming.  A CTA walks a contiguous run of
+// (column tile, plane) units -- column tile = 128 k x 16 j outputs -- and a
+// producer warp streams the input planes of that run (box 136 k x 18 j with
+// the halo, negative / past-the-end coordinates zero-filled by TMA) through
+// a kNS-deep shared-memory ring, several planes ahead of the math.  Each
+// input plane is read from shared memory once: it finishes the outputs of
+// the previous plane (its p-taps), adds its z-taps to the current plane and
+// starts the next plane (its m-taps).  Runs are balanced to +-1 plane over a
+// grid of exactly the resident CTAs (SMs x occupancy).
+constexpr int kTK = 128, kTJ = 16;          // output column tile
+constexpr int kBoxK = kTK + 8, kBoxJ = kTJ + 2;  // input box: k0-4 .. k0+131, j0-1 .. j0+16
+constexpr int kNS = 6;                       // planes in the ring
+constexpr uint32_t kSlotBytes = (kBoxK * kBoxJ * 4 + 127) / 128 * 128;
+constexpr int kConsumerWarps = kTJ / 2;      // warp w: output rows j0+2w, j0+2w+1; lane: 4 k
+constexpr int kS2Threads = 32 * (kConsumerWarps + 1);
+
+struct S2Params {
+  CUtensorMap map;
+  float* B;
+  int ni, nj, nk;
+  int tiles_k, tiles;   // column tiles along k, total column tiles
+  int64_t units;        // tiles * (ni - 2)
 };
 
-__device__ __forceinline__ Row6 load_row6(const float* __restrict__ A, size_t rowbase, int k0, int nk) {
-  Row6 r;
-  const float4 c = __ldg(reinterpret_cast<const float4*>(A + rowbase + k0));
-  r.v[0] = k0 > 0 ? __ldg(A + rowbase + k0 - 1) : 0.f;
-  r.v[1] = c.x;
-  r.v[2] = c.y;
-  r.v[3] = c.z;
-  r.v[4] = c.w;
-  r.v[5] = k0 + 4 < nk ? __ldg(A + rowbase + k0 + 4) : 0.f;
-  return r;
-}
+
 
 template <BenchId Bn, int V>
-__global__ void __launch_bounds__(128) conv3d_s2(const float* __restrict__ A, float* __restrict__ B, int ni, int nj,
-                                                 int nk) {
-  const int k0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  if (j <= 0 || j >= nj - 1 || k0 >= nk) return;
-  const size_t plane = (size_t)nj * nk;
-  const int i0 = 1 + blockIdx.z * kChunk, i1 = min(ni - 1, i0 + kChunk);
-  // rows (j-1, j, j+1) of planes i-1 and i
-  Row6 m[3], z[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    m[d] = load_row6(A, (size_t)(i0 - 1) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
-    z[d] = load_row6(A, (size_t)i0 * plane + (size_t)(j - 1 + d) * nk, k0, nk);
+__global__ void __launch_bounds__(kS2Threads) conv3d_s2(const __grid_constant__ S2Params p) {
+  extern __shared__ __align__(128) uint8_t c3_smem[];
+  __shared__ __align__(8) uint64_t full[kNS], empty[kNS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int planes = p.ni - 2;
+  const int64_t u0 = p.units * blockIdx.x / gridDim.x, u1 = p.units * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      tc::mbar_init(tc::smem_u32(&full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&empty[s]), kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  // plane i+1 rows are prefetched one iteration ahead (plane i+2 requested
-  // while plane i is computed): two planes of loads in flight per thread
-  Row6 p[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) p[d] = load_row6(A, (size_t)(i0 + 1) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
-  for (int i = i0; i < i1; ++i) {
-    Row6 q[3];
-    if (i + 2 < ni) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d) q[d] = load_row6(A, (size_t)(i + 2) * plane + (size_t)(j - 1 + d) * nk, k0, nk);
+  __syncthreads();
+  const uint32_t base = tc::smem_u32(c3_smem);
+
+  if (warp == kConsumerWarps) {
+    // ---- producer: every input plane of every segment of [u0, u1)
+    if (lane == 0) {
+      int n = 0;
+      for (int64_t u = u0; u < u1;) {
+        const int t = (int)(u / planes), i_begin = 1 + (int)(u % planes);
+        const int i_end = (int)(i_begin + (u1 - u) < (int64_t)planes + 1 ? i_begin + (u1 - u) : (int64_t)planes + 1);  // exclusive output plane
+        const int k0 = (t % p.tiles_k) * kTK, j0 = 1 + (t / p.tiles_k) * kTJ;
+        for (int q = i_begin - 1; q <= i_end; ++q, ++n) {
+          const int s = n % kNS;
+          tc::mbar_wait(tc::smem_u32(&empty[s]), ((n / kNS) & 1) ^ 1);
+          const uint32_t fb = tc::smem_u32(&full[s]);
+          tc::mbar_expect_tx(fb, kBoxK * kBoxJ * 4);
+          tma::load_3d(base + s * kSlotBytes, &p.map, k0 - 4, j0 - 1, q, fb);
+        }
+        u += i_end - i_begin;
+      }
     }
-    float out[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      // output k = k0 + e -> index e+1 in Row6; k-1 -> e, k+1 -> e+2
-      Taps t{m[0].v[e], m[0].v[e + 2], m[1].v[e + 2], m[2].v[e + 2], z[0].v[e + 1], z[1].v[e + 1], z[2].v[e + 1],
-             p[0].v[e], p[0].v[e + 2], p[1].v[e + 2], p[2].v[e + 2]};
-      out[e] = eval15(t);
-    }
-    float* brow = B + (size_t)i * plane + (size_t)j * nk;
-    if (k0 > 0 && k0 + 4 < nk) {
-      __stcs(reinterpret_cast<float4*>(brow + k0), make_float4(out[0], out[1], out[2], out[3]));
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (k0 + e > 0 && k0 + e < nk - 1) brow[k0 + e] = out[e];
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      m[d] = z[d];
-      z[d] = p[d];
-      p[d] = q[d];
-    }
+    return;
   }
+
+  // ---- consumers
+  int n = 0;
+  for (int64_t u = u0; u < u1;) {
+    const int t = (int)(u / planes), i_begin = 1 + (int)(u % planes);
+    const int i_end = (int)(i_begin + (u1 - u) < (int64_t)planes + 1 ? i_begin + (u1 - u) : (int64_t)planes + 1);
+    const int k0 = (t % p.tiles_k) * kTK, j0 = 1 + (t / p.tiles_k) * kTJ;
+    const int kq = k0 + 4 * lane;       // first of this thread's 4 k
+    const int jr = j0 + 2 * warp;       // first of this thread's 2 rows
+    float mz[2][4] = {}, mn[2][4] = {};
+    for (int q = i_begin - 1; q <= i_end; ++q, ++n) {
+      const int s = n % kNS;
+      tc::mbar_wait(tc::smem_u32(&full[s]), (n / kNS) & 1);
+      const float* slot = reinterpret_cast<const float*>(c3_smem + s * kSlotBytes);
+      // rows j-1 .. j+2 of the two output rows: smem rows 2w .. 2w+3
+      float v[4][6];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const float* row = slot + (2 * warp + rr) * kBoxK;
+        const float4 c = *reinterpret_cast<const float4*>(row + 4 + 4 * lane);
+        float left = __shfl_up_sync(0xffffffffu, c.w, 1);
+        float right = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (lane == 0) left = row[3];
+        if (lane == 31) right = row[4 + kTK];
+        v[rr][0] = left;
+        v[rr][1] = c.x;
+        v[rr][2] = c.y;
+        v[rr][3] = c.z;
+        v[rr][4] = c.w;
+        v[rr][5] = right;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&empty[s])) : "memory");
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        float out[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          // (j-1, k-1) (j-1, k+1) (j, k+1) (j+1, k+1) and (j-1, k) (j, k) (j+1, k)
+          const float xmm = v[r][e], xmp = v[r][e + 2], xzp = v[r + 1][e + 2], xpp = v[r + 2][e + 2];
+          const float xmz = v[r][e + 1], xzz = v[r + 1][e + 1], xpz = v[r + 2][e + 1];
+          const float P = c13 * xmm + c23 * xmm + c33 * xmm + c13 * xmp + c23 * xzp + c33 * xpp;
+          const float Z = c12 * xmz + c22 * xzz + c32 * xpz;
+          const float M = c11 * xmm + c21 * xmm + c31 * xmm + c11 * xmp + c21 * xzp + c31 * xpp;
+          out[e] = mz[r][e] + P;  // outputs of plane q-1 (valid for q > i_begin)
+          mz[r][e] = mn[r][e] + Z;
+          mn[r][e] = M;
+        }
+        const int i = q - 1, j = jr + r;
+        if (q > i_begin && j <= p.nj - 2 && kq < p.nk) {
+          float* brow = p.B + ((size_t)i * p.nj + j) * p.nk;
+          if (kq >= 1 && kq + 4 <= p.nk - 1) {
+            __stcs(reinterpret_cast<float4*>(brow + kq), make_float4(out[0], out[1], out[2], out[3]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (kq + e >= 1 && kq + e <= p.nk - 2) brow[kq + e] = out[e];
+          }
+        }
+      }
+    }
+    u += i_end - i_begin;
+  }
+}
+
+template <int V>
+void launch_s2(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(conv3d_s2<B_3DCONV, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kNS * kSlotBytes));
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv3d_s2<B_3DCONV, V>, kS2Threads, kNS * kSlotBytes);
+    grid = std::max(1, per_sm) * sms;
+  }
+  S2Params p;
+  if (!tma::make_map_3d(&p.map, A, nk, nj, ni, kBoxK, kBoxJ, 1)) {  // check() guarantees nk % 4 == 0
+    launch_failed("3DCONV stage 2: cuTensorMapEncodeTiled rejected the input plane map");
+    return;
+  }
+  p.B = B;
+  p.ni = ni;
+  p.nj = nj;
+  p.nk = nk;
+  p.tiles_k = (int)cdiv(nk, kTK);
+  p.tiles = p.tiles_k * (int)cdiv(nj - 2, kTJ);
+  p.units = (int64_t)p.tiles * (ni - 2);
+  const int g = (int)std::min<int64_t>(grid, p.units);
+  conv3d_s2<B_3DCONV, V><<<g, kS2Threads, kNS * kSlotBytes, s>>>(p);
 }
 
 template <int V>
@@ -196,8 +285,7 @@ struct Run {
       conv3d_s1<B_3DCONV, V><<<dim3(cdiv(nk, 32), cdiv(nj, 8), cdiv(ni - 2, kChunk)), dim3(32, 8), 0, s>>>(A, B, ni, nj,
                                                                                                     nk);
     } else {
-      conv3d_s2<B_3DCONV, V><<<dim3(cdiv(nk, 4 * 32), cdiv(nj, 4), cdiv(ni - 2, kChunk)), dim3(32, 4), 0, s>>>(
-          A, B, ni, nj, nk);
+      launch_s2<V>(A, B, ni, nj, nk, s);
     }
   }
 };

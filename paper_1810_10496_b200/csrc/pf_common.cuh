@@ -207,6 +207,17 @@ constexpr auto make_run_table(std::integer_sequence<int, Vs...>) {
 }
 
 // ---------------------------------------------------------------- launch helpers
+// Host-side launch failures inside a variant's run function (e.g. a TMA map
+// the driver refuses): recorded here and turned into PF_ECUDA by abi.cu right
+// after the run, so a variant never silently skips its kernel.
+inline thread_local const char* g_launch_error = nullptr;
+inline void launch_failed(const char* why) { g_launch_error = why; }
+inline const char* take_launch_error() {
+  const char* w = g_launch_error;
+  g_launch_error = nullptr;
+  return w;
+}
+
 inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 // 32x8 blocks: the PolyBench/GPU DIM_THREAD_BLOCK_X/Y default

@@ -168,6 +168,43 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Epilogue of one warp: TMEM lanes (tile rows row0 .. row0+31) x ncols
+// accumulator columns starting at TMEM column 0 / output column col0.
+// tcgen05.ld gives lane = row, register j = column; the 32x32 block is
+// transposed through a padded per-warp shared buffer (33-float rows: both
+// phases conflict-free) so every global access is one 128-byte row segment
+// (lane = column) instead of 32 rows x 4 bytes.
+//   split:  D += alpha * acc          (D pre-scaled by beta; red.global.add)
+//   else:   D  = alpha * acc + beta * Cin
+__device__ __forceinline__ void epilogue_rows32(uint32_t taddr, int ncols, int row0, int col0, int M, int N,
+                                                float alpha, float beta, const float* Cin, int ldc, float* D,
+                                                int ldd, bool split, float* stage, int lane) {
+#pragma unroll 1
+  for (int c = 0; c < ncols / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + (uint32_t)(c * 32), r);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = __uint_as_float(r[j]);
+    __syncwarp();
+    const int col = col0 + c * 32 + lane;
+    if (col < N) {
+#pragma unroll 4
+      for (int rr = 0; rr < 32; ++rr) {
+        const int row = row0 + rr;
+        if (row >= M) break;
+        const float v = alpha * stage[rr * 33 + lane];
+        float* d = D + (size_t)row * ldd + col;
+        if (split) {
+          atomicAdd(d, v);
+        } else {
+          *d = beta != 0.f ? fmaf(beta, Cin[(size_t)row * ldc + col], v) : v;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace tc
 
 // Pack op(X) (R x K logical, rows = M for A / N for B) into hi/lo K-major
@@ -305,35 +342,12 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_kernel(TcParams p) {
   }
   __syncwarp();
 
-  // Epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31.
+  // Epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31; the idle
+  // stage ring (all MMAs retired) holds the per-warp transpose buffers.
   tc::mbar_wait(tc::smem_u32(&accum_bar), 0);
   tc::fence_after();
-  const int row = mb * kTcBM + warp * 32 + lane;
-#pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    uint32_t r[32];
-    tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32), r);
-    const int col0 = nb * BN + c * 32;
-    if (row < p.M) {
-      float* drow = p.D + (size_t)row * p.ldd;
-      const float* crow = p.Cin + (size_t)row * p.ldc;
-      if (split) {  // D was pre-scaled by beta; add this k-range's partial
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (col0 + j < p.N) atomicAdd(drow + col0 + j, p.alpha * __uint_as_float(r[j]));
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = col0 + j;
-          if (col < p.N) {
-            float v = p.alpha * __uint_as_float(r[j]);
-            if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
-            drow[col] = v;
-          }
-        }
-      }
-    }
-  }
+  tc::epilogue_rows32(tmem + ((uint32_t)(warp * 32) << 16), BN, mb * kTcBM + warp * 32, nb * BN, p.M, p.N, p.alpha,
+                      p.beta, p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + warp * 32 * 33, lane);
   tc::fence_before();
   __syncthreads();
   if (warp == 2) {

@@ -26,8 +26,7 @@
 #pragma once
 #include "pf_common.cuh"
 #include "tc_gemm.cuh"
-
-#include <cuda.h>
+#include "tma_map.cuh"
 
 #include <cstdlib>
 #include <cstring>
@@ -55,6 +54,7 @@ struct TmaParams {
   int upper_only;
   uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides / k-step advance (bytes)
   int idesc_override;                 // probe only: -1 auto, else (a_major | b_major << 1)
+  int diag;                           // diagnostics only (PF_TC_DIAG): 1 skip lo split, 2 skip MMAs, 4 skip loads, 8 skip epilogue
 };
 
 namespace tma {
@@ -144,6 +144,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
         const uint32_t ph = (i / kTmaStages) & 1;
         tc::mbar_wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
         const uint32_t fb = tc::smem_u32(&full_bar[s]);
+        if (p.diag & 4) {  // diagnostics: no operand loads
+          tma::mbar_arrive(fb);
+          continue;
+        }
         tc::mbar_expect_tx(fb, 2 * kTmaTileBytes);
         const bool second = kb >= p.kb1;
         const CUtensorMap* ma = second ? &p.ta2 : &p.ta;
@@ -182,6 +186,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
           const uint64_t bhi = tma::desc(base + kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
           const uint64_t alo = tma::desc(base + 2 * kTmaTileBytes + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
           const uint64_t blo = tma::desc(base + 3 * kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
+          if (p.diag & 2) continue;
           tc::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
           tc::mma_tf32(tmem, ahi, blo, id, 1u);
           tc::mma_tf32(tmem, ahi, bhi, id, 1u);
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       const float4* raw = reinterpret_cast<const float4*>(smem + (size_t)s * kTmaStageBytes);
       float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * kTmaStageBytes + 2 * kTmaTileBytes);
 #pragma unroll 4
-      for (int q = ct; q < (int)(2 * kTmaTileBytes / 16); q += 128) {
+      for (int q = ct; q < ((p.diag & 1) ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
         const float4 v = raw[q];
         lo[q] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y), v.z - tma::trunc_tf32(v.z),
                             v.w - tma::trunc_tf32(v.w));
@@ -210,36 +215,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(tc::smem_u32(&ready_bar[s]));
     }
-    // ---- epilogue: TMEM lanes 32*(warp%4) .. +31 are tile rows
+    // ---- epilogue: TMEM lanes 32*(warp%4) .. +31 are tile rows (coalesced
+    // through the idle stage ring, see tc::epilogue_rows32)
     tc::mbar_wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
     const int quad = warp & 3;
-    const int row = m0 + quad * 32 + lane;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t r[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32), r);
-      const int col0 = n0 + c * 32;
-      if (row < p.M) {
-        float* drow = p.D + (size_t)row * p.ldd;
-        if (split) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < p.N) atomicAdd(drow + col0 + j, p.alpha * __uint_as_float(r[j]));
-        } else {
-          const float* crow = p.Cin + (size_t)row * p.ldc;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + j;
-            if (col < p.N) {
-              float v = p.alpha * __uint_as_float(r[j]);
-              if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
-              drow[col] = v;
-            }
-          }
-        }
-      }
-    }
+    if (!(p.diag & 8))
+      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+                          p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
   }
   tc::fence_before();
   __syncthreads();
@@ -371,6 +354,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
         const uint32_t ph = (i / kTmaStages) & 1;
         tc2::wait(tc::smem_u32(&empty_bar[s]), ph ^ 1);
         const uint32_t fb = tc::smem_u32(&full_bar[s]);
+        if (p.diag & 4) {  // diagnostics: no operand loads
+          tma::mbar_arrive(fb);
+          continue;
+        }
         tc::mbar_expect_tx(fb, 2 * kTmaTileBytes);
         const bool second = kb >= p.kb1;
         const CUtensorMap* ma = second ? &p.ta2 : &p.ta;
@@ -408,6 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
           const uint64_t bhi = tma::desc(base + kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
           const uint64_t alo = tma::desc(base + 2 * kTmaTileBytes + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
           const uint64_t blo = tma::desc(base + 3 * kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
+          if (p.diag & 2) continue;
           tc2::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
           tc2::mma_tf32(tmem, ahi, blo, id, 1u);
           tc2::mma_tf32(tmem, ahi, bhi, id, 1u);
@@ -426,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       const float4* raw = reinterpret_cast<const float4*>(smem + (size_t)s * kTmaStageBytes);
       float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * kTmaStageBytes + 2 * kTmaTileBytes);
 #pragma unroll 4
-      for (int q = ct; q < (int)(2 * kTmaTileBytes / 16); q += 128) {
+      for (int q = ct; q < ((p.diag & 1) ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
         const float4 v = raw[q];
         lo[q] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y), v.z - tma::trunc_tf32(v.z),
                             v.w - tma::trunc_tf32(v.w));
@@ -435,35 +423,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       __syncwarp();
       if (lane == 0) tc2::arrive_remote(tc2::peer_addr(tc::smem_u32(&ready_bar[s]), 0));
     }
+    // all MMAs of the pair (which read this CTA's ring) have retired once
+    // accum fires, so the ring holds the epilogue transpose buffers
     tc2::wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
     const int quad = warp & 3;
-    const int row = m0 + quad * 32 + lane;
-#pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
-      uint32_t r[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32), r);
-      const int col0 = n0 + c * 32;
-      if (row < p.M) {
-        float* drow = p.D + (size_t)row * p.ldd;
-        if (split) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < p.N) atomicAdd(drow + col0 + j, p.alpha * __uint_as_float(r[j]));
-        } else {
-          const float* crow = p.Cin + (size_t)row * p.ldc;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = col0 + j;
-            if (col < p.N) {
-              float v = p.alpha * __uint_as_float(r[j]);
-              if (p.beta != 0.f) v = fmaf(p.beta, crow[col], v);
-              drow[col] = v;
-            }
-          }
-        }
-      }
-    }
+    if (!(p.diag & 8))
+      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+                          p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
   }
   tc::fence_before();
   tc2::cluster_sync();
@@ -474,22 +441,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
 
 // ---------------------------------------------------------------- host side
 namespace tma {
-
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-inline EncodeFn encoder() {
-  static EncodeFn fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<EncodeFn>(f);
-  }();
-  return fn;
-}
 
 // 2-D fp32 tensor map over X[outer][inner] (row pitch ld elements), box
 // {box_inner, box_outer}, out-of-bounds reads as zero.  K-major tiles use
@@ -584,6 +535,11 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
   p.mn_sbo = tma_probe().sbo;
   p.mn_kstep = tma_probe().kstep;
   p.idesc_override = tma_probe().idesc_override;
+  static const int diag = [] {
+    const char* e = std::getenv("PF_TC_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.diag = diag;
   p.a_mn = a.ta ? 1 : 0;
   p.b_mn = a.tb ? 0 : 1;
   if (!tma::operand_map(&p.ta, a.A, p.a_mn, a.M, a.K, a.lda)) return false;

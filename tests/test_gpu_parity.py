@@ -145,3 +145,30 @@ def test_tensor_core_tiles_match_oracle(bench, gpu_backend):
                 if not ok:
                     failures.append(f"{dims} v{v} out{k}: worst/tol={worst:.3g}")
     assert not failures, "\n".join(failures)
+
+
+# Stencil tiling edges: partial 128-wide k tiles, j tiles and i runs that end
+# mid-tile, tiny volumes where a run spans several column tiles.
+STENCIL_SIZES = {"3DCONV": [(37, 45, 132), (9, 20, 8), (64, 33, 260)], "2DCONV": [(67, 516), (5, 8)]}
+
+
+@pytest.mark.parametrize("bench", [b for b in STENCIL_SIZES if b in BUILT])
+def test_stencil_tiles_match_oracle(bench, gpu_backend):
+    from paper_1810_10496_b200.backend import b200
+
+    fam = b200.family(bench)
+    failures, ran = [], 0
+    for dims in STENCIL_SIZES[bench]:
+        ref = orc.reference(bench, dims, False, gpu_backend.seed, 2)
+        for v in range(len(fam.knobs)):
+            if fam.knobs[v][0] == 0 or not gpu_backend._supported(bench, v, dims):
+                continue
+            ws = gpu_backend.workspace(bench, dims, False, 2)
+            ws.run(v, samples=1, batch=1, restore=True, flush=False)
+            ran += 1
+            for k, (g, r) in enumerate(zip(ws.outputs(), ref)):
+                ok, worst = _close(g, r)
+                if not ok:
+                    failures.append(f"{dims} v{v} [{fam.key(v)}] out{k}: worst/tol={worst:.3g}")
+    assert ran > 0
+    assert not failures, "\n".join(failures)

@@ -30,6 +30,15 @@ def suite(tmp_path_factory):
     return cases, ToolchainBackend(spec), be
 
 
+def _same(a, b):
+    """Report values round-trip bit-exactly (repr); variants whose column
+    reductions use float atomics (fused BLAS-2) may differ run to run in the
+    last bits, so the bar is 1e-6 relative, far inside the 1e-4 parity bar."""
+    assert len(a) == len(b)
+    for x, y in zip(a, b):
+        assert abs(x - y) <= 1e-6 * max(abs(x), abs(y), 1e-30), (x, y)
+
+
 def test_runner_outputs_equal_in_process(suite):
     cases, tc, be = suite
     orders = [PhaseOrder(), PhaseOrder.of("cfl-anders-aa", "licm", "loop-unroll", "bb-vectorize"),
@@ -43,10 +52,10 @@ def test_runner_outputs_equal_in_process(suite):
             ra = tc.execute(case, order, a.artifact, InputKind.VALIDATION)
             rb = be.execute(own, order, b.artifact, InputKind.VALIDATION)
             assert ra.status is rb.status is ExecutionStatus.VALID
-            assert ra.outputs == rb.outputs  # repr round-trip: bit-exact
+            _same(ra.outputs, rb.outputs)
             ra = tc.execute(case, order, a.artifact, InputKind.VALIDATION, random_input_index=3)
             rb = be.execute(own, order, b.artifact, InputKind.VALIDATION, random_input_index=3)
-            assert ra.outputs == rb.outputs
+            _same(ra.outputs, rb.outputs)
             m = tc.execute(case, order, a.artifact, InputKind.MEASUREMENT)
             assert m.status is ExecutionStatus.VALID and m.wall_time > 0 and m.outputs == ()
 
