@@ -8,12 +8,18 @@
 //          the paper's 5.4x CORR case).
 // stage 1  row-split column statistics (atomics) and the Gram matrix D^T D
 //          as an upper-triangle tiled SIMT GEMM + mirror.
-// stage 2  the Gram matrix on tcgen05 3xTF32 (MN-major operands straight
-//          from the 1-based array) + mirror.
+// stage 2  the normalisation pass also writes the centred (scaled) data
+//          transposed into an aligned m x n scratch (32x32 shared-memory
+//          tiles), so the Gram matrix X X^T runs on the TMA-fed tcgen05
+//          3xTF32 kernel exactly like SYRK (upper-triangle tiles, K-major
+//          operands, TMA epilogue into an aligned m x m scratch); one tiled
+//          pass then scatters it into the 1-based symmat with the mirror (and
+//          CORR's unit diagonal) folded in.
 #pragma once
 #include "pf_common.cuh"
 #include "simt_gemm.cuh"
 #include "tc_gemm.cuh"
+#include "tc_tma.cuh"
 
 #include <algorithm>
 
@@ -162,6 +168,63 @@ inline void launch_colstat(const float* data, const float* mean, float* out, int
   finalize_stat<Bn, V, kPass><<<cdiv(m, 256), 256, 0, s>>>(out, m);
 }
 
+// Stage 2: normalise in place (reduce_s0's arithmetic) and write the result
+// transposed: xt[(j-1) * ldx + i-1] = data[i][j].  Block (32, 8), 32x32 tile.
+template <BenchId Bn, int V, bool kCorr>
+__global__ void __launch_bounds__(256) reduce_transpose(const float* __restrict__ mean, const float* __restrict__ stdv,
+                                                        float* data, float* __restrict__ xt, int m, int n,
+                                                        int ldx) {
+  __shared__ float t[32][33];
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+#pragma unroll
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int i = i0 + r + 1, j = j0 + threadIdx.x + 1;
+    if (i <= n && j <= m) {
+      float* p = data + (size_t)i * (m + 1) + j;
+      float v = *p - mean[j];
+      if constexpr (kCorr) v /= (sqrtf(kFloatN) * stdv[j]);
+      *p = v;
+      t[r][threadIdx.x] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int j = j0 + r, i = i0 + threadIdx.x;
+    if (j < m && i < n) xt[(size_t)j * ldx + i] = t[threadIdx.x][r];
+  }
+}
+
+// symmat[1 + r][1 + c] = G[min(r,c)][max(r,c)] (pitch ldg) (only G's upper triangle is
+// computed); CORR's diagonal is 1.  Block (32, 8), 32x32 tile.
+template <BenchId Bn, int V, bool kCorr>
+__global__ void __launch_bounds__(256) sym_scatter(const float* __restrict__ G, int ldg, float* sym, int m) {
+  __shared__ float t[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const bool lower = r0 > c0;  // tile strictly below the diagonal blocks: read the transposed tile
+#pragma unroll
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int gr = (lower ? c0 : r0) + k, gc = (lower ? r0 : c0) + threadIdx.x;
+    if (gr < m && gc < m) t[k][threadIdx.x] = G[(size_t)gr * ldg + gc];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int r = r0 + k, c = c0 + threadIdx.x;
+    if (r < m && c < m) {
+      float v;
+      if (lower)
+        v = t[threadIdx.x][k];
+      else if (r <= c)
+        v = t[k][threadIdx.x];
+      else
+        v = t[threadIdx.x][k];  // diagonal tile, lower half: mirror within the tile
+      if (kCorr && r == c) v = 1.0f;
+      sym[(size_t)(r + 1) * (m + 1) + (c + 1)] = v;
+    }
+  }
+}
+
 // One variant run.  arrays: data, mean, [std,] symmat
 template <BenchId Bn, int V, bool kCorr, int kStage, int kStore, int kUnroll, int kLsr>
 inline void run(Workspace& ws, cudaStream_t s) {
@@ -178,16 +241,26 @@ inline void run(Workspace& ws, cudaStream_t s) {
   } else {
     launch_colstat<Bn, V, 0>(data, nullptr, mean, m, n, s);
     if constexpr (kCorr) launch_colstat<Bn, V, 1>(data, mean, stdv, m, n, s);
+    if constexpr (kStage == 2) {
+      // 16-byte pitches for the TMA maps (K tail beyond n reads as zero)
+      const int np = (n + 3) / 4 * 4, mp = (m + 3) / 4 * 4;
+      float* xt = ws.ensure_scratch(((size_t)m * np + (size_t)m * mp) * sizeof(float));
+      float* G = xt + (size_t)m * np;
+      reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, 32), cdiv(n, 32)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt, m,
+                                                                                           n, np);
+      const TcGemmArgs g{m, m, n, 1.f, 0.f, xt, np, false, xt, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
+      if (!launch_tc_tma<Bn, V>(g, s)) {
+        launch_failed("CORR/COVAR stage 2: TMA operand maps rejected");
+        return;
+      }
+      sym_scatter<Bn, V, kCorr><<<dim3(cdiv(m, 32), cdiv(m, 32)), dim3(32, 8), 0, s>>>(G, mp, sym, m);
+      return;
+    }
     reduce_s0<Bn, V, kCorr><<<dim3(cdiv(m, kBX), cdiv(n, kBY)), dim3(kBX, kBY), 0, s>>>(mean, stdv, data, m, n);
     const float* d1 = data + (m + 1) + 1;  // data[1][1]
     float* s1 = sym + (m + 1) + 1;         // symmat[1][1]
-    if constexpr (kStage == 1) {
-      launch_simt_gemm<Bn, V, true, false, false>(
-          SimtGemmArgs{m, m, n, 1.f, 0.f, d1, m + 1, d1, m + 1, nullptr, nullptr, nullptr, m + 1, s1, m + 1, 1}, s);
-    } else {
-      launch_tc_gemm<Bn, V>(ws, TcGemmArgs{m, m, n, 1.f, 0.f, d1, m + 1, true, d1, m + 1, false, nullptr, nullptr,
-                                           nullptr, m + 1, s1, m + 1, 1}, s);
-    }
+    launch_simt_gemm<Bn, V, true, false, false>(
+        SimtGemmArgs{m, m, n, 1.f, 0.f, d1, m + 1, d1, m + 1, nullptr, nullptr, nullptr, m + 1, s1, m + 1, 1}, s);
     launch_mirror<Bn, V>(s1, m, m + 1, s);
     if constexpr (kCorr) set_unit_diag<Bn, V><<<cdiv(m, 256), 256, 0, s>>>(sym, m);
   }
@@ -196,8 +269,8 @@ inline void run(Workspace& ws, cudaStream_t s) {
 inline int64_t launches(bool corr, int stage, int64_t m, int64_t n) {
   if (stage == 0) return corr ? 4 : 3;
   const int64_t stats = corr ? 4 : 2;
-  const int64_t gram = stage == 1 ? 1 : tc_gemm_launches(m, m, n);
-  return stats + 1 + gram + 1 + (corr ? 1 : 0);
+  if (stage == 2) return stats + 1 + tc_tma_launches(m, m, n, false, true) + 1;
+  return stats + 1 + 1 + 1 + (corr ? 1 : 0);
 }
 
 }  // namespace corrcov

@@ -12,6 +12,7 @@
 #include "tma_map.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace pf {
 namespace {
@@ -244,6 +245,133 @@ __global__ void __launch_bounds__(kS2Threads) conv3d_s2(const __grid_constant__ 
   }
 }
 
+// Stage 2, direct form: no shared memory.  A thread owns 4 consecutive k
+// (one float4) x kR rows j and streams a chunk of kCH output planes along i.
+// Every input plane q is consumed once as it arrives (its p-taps finish
+// output q-1, its z-taps extend output q, its m-taps start output q+1), so
+// only two partial-sum planes stay in registers; the loads of plane q + kPD
+// are issued before plane q is consumed (register prefetch ring of kPD
+// planes), keeping kPD x (kR + 2) x 16 B of loads in flight per thread.
+// The repeated PolyBench taps are folded ((c11+c21+c31) A[i-1][j-1][k-1],
+// (c13+c23+c33) A[i+1][j-1][k-1]): 11 FMAs per output.
+
+template <int R, int KV>
+struct PlaneRows {
+  float v[R + 2][4 * KV + 2];  // rows j-1 .. j+R, columns k-1 .. k+4KV
+};
+
+// Loads of one input plane: row offsets and halo offsets are fixed per
+// thread (clamped once, outside the plane loop), so the loop body carries no
+// predicates -- a clamped halo only ever feeds a border output that is not
+// stored.
+template <int R, int KV>
+__device__ __forceinline__ void load_rows(PlaneRows<R, KV>& P, const float* __restrict__ plane,
+                                          const int (&roff)[R + 2], int offL, int offR) {
+#pragma unroll
+  for (int rr = 0; rr < R + 2; ++rr) {
+    const float* rp = plane + roff[rr];
+    P.v[rr][0] = __ldg(rp + offL);
+#pragma unroll
+    for (int h = 0; h < KV; ++h) {
+      const float4 c = __ldcs(reinterpret_cast<const float4*>(rp) + h);
+      P.v[rr][4 * h + 1] = c.x;
+      P.v[rr][4 * h + 2] = c.y;
+      P.v[rr][4 * h + 3] = c.z;
+      P.v[rr][4 * h + 4] = c.w;
+    }
+    P.v[rr][4 * KV + 1] = __ldg(rp + offR);
+  }
+}
+
+template <BenchId Bn, int V, int R, int PD, int CH, int TX, int TY, int KV>
+__global__ void __launch_bounds__(TX * TY) conv3d_s2d(const float* __restrict__ A, float* __restrict__ B, int ni,
+                                                      int nj, int nk) {
+  constexpr int W = 4 * KV;  // outputs along k per thread
+  const int kq = W * (blockIdx.x * TX + threadIdx.x);
+  const int jr = 1 + (blockIdx.y * TY + threadIdx.y) * R;
+  if (kq >= nk || jr > nj - 2) return;
+  const int i0 = 1 + blockIdx.z * CH, i1 = min(ni - 1, i0 + CH);  // outputs [i0, i1), inputs i0-1 .. i1
+  const int plane = nj * nk;                                      // < 2^31 (checked on the host)
+  int roff[R + 2];
+#pragma unroll
+  for (int rr = 0; rr < R + 2; ++rr) roff[rr] = min(jr - 1 + rr, nj - 1) * nk + kq;
+  const int offL = kq > 0 ? -1 : 0, offR = kq + W < nk ? W : W - 1;
+  const bool full = kq >= 1 && kq + W <= nk - 1;
+  constexpr float cM = c11 + c21 + c31, cP = c13 + c23 + c33;
+  const float* src = A + (size_t)(i0 - 1) * plane;
+  float* dst = B + (size_t)i0 * plane + jr * nk + kq;  // row jr of output plane i0
+  const int nq = i1 - i0 + 2;
+  PlaneRows<R, KV> ring[PD];
+#pragma unroll
+  for (int d = 0; d < PD; ++d)
+    if (d < nq) load_rows<R, KV>(ring[d], src + d * plane, roff, offL, offR);
+  float mz[R][W], mn[R][W];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int e = 0; e < W; ++e) mz[r][e] = mn[r][e] = 0.f;
+  for (int q0 = 0; q0 < nq; q0 += PD) {
+#pragma unroll
+    for (int d = 0; d < PD; ++d) {
+      const int q = q0 + d;
+      if (q >= nq) break;
+      const PlaneRows<R, KV>& cur = ring[d];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float out[W];
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+          const float xmm = cur.v[r][e], xmz = cur.v[r][e + 1], xmp = cur.v[r][e + 2];
+          const float xzz = cur.v[r + 1][e + 1], xzp = cur.v[r + 1][e + 2];
+          const float xpz = cur.v[r + 2][e + 1], xpp = cur.v[r + 2][e + 2];
+          // this plane as i+1 of output q-1, as i of output q, as i-1 of output q+1
+          out[e] = fmaf(c33, xpp, fmaf(c23, xzp, fmaf(c13, xmp, fmaf(cP, xmm, mz[r][e]))));
+          mz[r][e] = fmaf(c32, xpz, fmaf(c22, xzz, fmaf(c12, xmz, mn[r][e])));
+          mn[r][e] = fmaf(c31, xpp, fmaf(c21, xzp, fmaf(c11, xmp, cM * xmm)));
+        }
+        if (q >= 2 && jr + r <= nj - 2) {  // relative input q finishes output plane i0 + q - 2
+          float* o = dst + (size_t)(q - 2) * plane + r * nk;
+          if (full) {
+#pragma unroll
+            for (int h = 0; h < KV; ++h)
+              __stcs(reinterpret_cast<float4*>(o) + h,
+                     make_float4(out[4 * h], out[4 * h + 1], out[4 * h + 2], out[4 * h + 3]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < W; ++e)
+              if (kq + e >= 1 && kq + e <= nk - 2) o[e] = out[e];
+          }
+        }
+      }
+      // the slot is free once consumed: refill it PD planes ahead
+      if (q + PD < nq) load_rows<R, KV>(ring[d], src + (size_t)(q + PD) * plane, roff, offL, offR);
+    }
+  }
+}
+
+template <int V, int R, int PD, int CH, int TX, int TY, int KV>
+void launch_s2d(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s) {
+  if constexpr (KV > 1) {
+    if (nk % (4 * KV)) {  // rows must hold whole KV-float4 groups
+      launch_s2d<V, R, PD, CH, TX, TY, 1>(A, B, ni, nj, nk, s);
+      return;
+    }
+  }
+  conv3d_s2d<B_3DCONV, V, R, PD, CH, TX, TY, KV><<<dim3(cdiv(nk, 4 * KV * TX), cdiv(nj - 2, TY * R), cdiv(ni - 2, CH)),
+                                                   dim3(TX, TY), 0, s>>>(A, B, ni, nj, nk);
+}
+
+// PF_C3 (A/B runs): "t" = TMA plane-streaming kernel, "0".."3" = direct-form
+// configurations; default = direct form 0.
+inline int c3_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("PF_C3");
+    if (!e || !e[0]) return 0;
+    return e[0] == 't' ? -1 : std::atoi(e);
+  }();
+  return m;
+}
+
 template <int V>
 void launch_s2(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s) {
   static int grid = 0;
@@ -284,8 +412,19 @@ struct Run {
     } else if constexpr (K.stage == 1) {
       conv3d_s1<B_3DCONV, V><<<dim3(cdiv(nk, 32), cdiv(nj, 8), cdiv(ni - 2, kChunk)), dim3(32, 8), 0, s>>>(A, B, ni, nj,
                                                                                                     nk);
-    } else {
+    } else if ((int64_t)nj * nk >= (int64_t(1) << 31)) {  // int32 plane offsets in the direct form
       launch_s2<V>(A, B, ni, nj, nk, s);
+    } else {
+      switch (c3_mode()) {
+        case -1: launch_s2<V>(A, B, ni, nj, nk, s); break;
+        case 1: launch_s2d<V, 4, 2, 32, 64, 1, 1>(A, B, ni, nj, nk, s); break;
+        case 2: launch_s2d<V, 2, 2, 32, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        case 3: launch_s2d<V, 2, 3, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        case 4: launch_s2d<V, 4, 2, 16, 64, 1, 1>(A, B, ni, nj, nk, s); break;
+        case 5: launch_s2d<V, 2, 2, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        case 6: launch_s2d<V, 3, 2, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        default: launch_s2d<V, 2, 2, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+      }
     }
   }
 };

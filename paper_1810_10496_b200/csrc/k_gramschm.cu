@@ -17,6 +17,7 @@
 #include "pf_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace pf {
 namespace {
@@ -294,6 +295,204 @@ void launch_panel(Workspace& ws, cudaStream_t s) {
   cudaLaunchCooperativeKernel((const void*)gs_panel<Bn, V>, dim3(grid), dim3(kPanelThreads), args, panel_smem(m), s);
 }
 
+// ---- stage 2, vec=1 (m <= 2048): persistent register-resident panels with
+// panel-granular hand-over.  CTA b owns columns [16b, 16b+16); warp w holds
+// panel columns 2w, 2w+1 in registers (lane: rows 128*(t/4) + 4*lane + t%4,
+// t < 64; rows >= m are zero and stay zero).  The arithmetic per column is
+// exactly the per-column kernel's (MGS: r = q_k . a_j on the current a_j, then
+// a_j -= r q_k, k ascending); only the synchronisation changes: CTA b waits
+// once per earlier PANEL (flag[p], release/acquire) and applies that panel's
+// 16 q vectors back to back, q_{k+1} prefetched from L2 into registers while
+// q_k is applied (one block barrier per q, double-buffered in shared memory),
+// then factors its own panel and publishes its 16 q vectors (qbuf, 2048-row
+// stride) with one flag.  Q = A * (1 / R[k][k]) (reciprocal once per column).
+constexpr int kP2Rows = 2048;  // max m: 64 rows per lane
+
+// Warp dot product of two 64-row lane slices: 4 independent FMA chains, then
+// the butterfly sum.
+__device__ __forceinline__ float dot64(const float (&x)[64], const float (&y)[64]) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 64; i += 4) {
+    s0 = fmaf(x[i], y[i], s0);
+    s1 = fmaf(x[i + 1], y[i + 1], s1);
+    s2 = fmaf(x[i + 2], y[i + 2], s2);
+    s3 = fmaf(x[i + 3], y[i + 3], s3);
+  }
+  return warp_sum((s0 + s1) + (s2 + s3));
+}
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict__ A, float* __restrict__ R,
+                                                              float* __restrict__ Q, float* __restrict__ qbuf,
+                                                              int* __restrict__ flags, int m, int n) {
+  __shared__ __align__(16) float qs[2][kP2Rows];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int b = blockIdx.x, c0 = b * kPanelW, w = min(kPanelW, n - c0);
+  float* st = &qs[0][0];  // staging for the panel load / store: 128 rows x 17
+  float a[2][64];
+
+  // ---- load the panel (coalesced 16-float row segments through shared memory)
+#pragma unroll
+  for (int P = 0; P < kP2Rows / 128; ++P) {
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int idx = t + 256 * e, row = 128 * P + idx / 16, col = idx % 16;
+      st[(idx / 16) * 17 + col] = (row < m && col < w) ? A[(size_t)row * n + c0 + col] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) a[c][4 * P + e] = st[(4 * lane + e) * 17 + 2 * warp + c];
+  }
+  __syncthreads();
+
+  int step = 0;
+  // ---- apply earlier panels
+  for (int pb = 0; pb < b; ++pb) {
+    if (t == 0)
+      while (ld_acquire(flags + pb) == 0) {
+      }
+    __syncthreads();
+    const float* qp = qbuf + (size_t)pb * kPanelW * kP2Rows;
+    float4 pre0 = __ldcg(reinterpret_cast<const float4*>(qp) + t);
+    float4 pre1 = __ldcg(reinterpret_cast<const float4*>(qp) + 256 + t);
+    for (int kk = 0; kk < kPanelW; ++kk, ++step) {
+      const int k = pb * kPanelW + kk;
+      float* qb = qs[step & 1];
+      reinterpret_cast<float4*>(qb)[t] = pre0;
+      reinterpret_cast<float4*>(qb)[256 + t] = pre1;
+      if (kk + 1 < kPanelW) {
+        pre0 = __ldcg(reinterpret_cast<const float4*>(qp + (size_t)(kk + 1) * kP2Rows) + t);
+        pre1 = __ldcg(reinterpret_cast<const float4*>(qp + (size_t)(kk + 1) * kP2Rows) + 256 + t);
+      }
+      __syncthreads();
+      float q[64];
+#pragma unroll
+      for (int g = 0; g < 16; ++g) {
+        const float4 v = reinterpret_cast<const float4*>(qb)[32 * g + lane];
+        q[4 * g] = v.x;
+        q[4 * g + 1] = v.y;
+        q[4 * g + 2] = v.z;
+        q[4 * g + 3] = v.w;
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (2 * warp + c >= w) continue;
+        float r = dot64(q, a[c]);
+        if (lane == 0) R[(size_t)k * n + c0 + 2 * warp + c] = r;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) a[c][i] = fmaf(-q[i], r, a[c][i]);
+      }
+    }
+  }
+
+  // ---- factor the own panel
+  float rdiag[2] = {1.f, 1.f};  // 1 / R[k][k] of the two own columns
+  for (int kk = 0; kk < w; ++kk, ++step) {
+    const int k = c0 + kk;
+    float* qb = qs[step & 1];
+    if (warp == kk / 2) {
+      // the pivot column's register slice is selected by a compile-time index
+      // (a runtime a[kk & 1] would demote the whole panel to local memory)
+      auto pivot = [&](float(&col)[64], float& rinv) {
+        const float rkk = sqrtf(dot64(col, col));
+        const float inv = 1.0f / rkk;
+        rinv = inv;
+        float* qg = qbuf + (size_t)k * kP2Rows;
+#pragma unroll
+        for (int g = 0; g < 16; ++g) {
+          const int row = 128 * g + 4 * lane;
+          float4 v;
+          v.x = row < m ? col[4 * g] * inv : 0.f;
+          v.y = row + 1 < m ? col[4 * g + 1] * inv : 0.f;
+          v.z = row + 2 < m ? col[4 * g + 2] * inv : 0.f;
+          v.w = row + 3 < m ? col[4 * g + 3] * inv : 0.f;
+          reinterpret_cast<float4*>(qb)[32 * g + lane] = v;
+          reinterpret_cast<float4*>(qg)[32 * g + lane] = v;
+        }
+        if (lane == 0) R[(size_t)k * n + k] = rkk;
+      };
+      if (kk & 1)
+        pivot(a[1], rdiag[1]);
+      else
+        pivot(a[0], rdiag[0]);
+    }
+    __syncthreads();
+    float q[64];
+#pragma unroll
+    for (int g = 0; g < 16; ++g) {
+      const float4 v = reinterpret_cast<const float4*>(qb)[32 * g + lane];
+      q[4 * g] = v.x;
+      q[4 * g + 1] = v.y;
+      q[4 * g + 2] = v.z;
+      q[4 * g + 3] = v.w;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int jj = 2 * warp + c;
+      if (jj >= w || jj <= kk) continue;
+      float r = dot64(q, a[c]);
+      if (lane == 0) R[(size_t)k * n + c0 + jj] = r;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) a[c][i] = fmaf(-q[i], r, a[c][i]);
+    }
+  }
+  // ---- publish the panel's q vectors
+  __threadfence();
+  __syncthreads();
+  if (t == 0) st_release(flags + b, 1);
+
+  // ---- write back A (final columns) and Q = A / R[k][k] (coalesced through shared memory)
+#pragma unroll 1
+  for (int which = 0; which < 2; ++which) {
+    float* dst = which ? Q : A;
+#pragma unroll
+    for (int P = 0; P < kP2Rows / 128; ++P) {
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          st[(4 * lane + e) * 17 + 2 * warp + c] = which ? a[c][4 * P + e] * rdiag[c] : a[c][4 * P + e];
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int idx = t + 256 * e, row = 128 * P + idx / 16, col = idx % 16;
+        if (row < m && col < w) dst[(size_t)row * n + c0 + col] = st[(idx / 16) * 17 + col];
+      }
+    }
+  }
+}
+
+template <BenchId Bn, int V>
+void launch_panel2(Workspace& ws, cudaStream_t s) {
+  const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
+  float* scratch = ws.ensure_scratch((size_t)n * kP2Rows * sizeof(float) + (size_t)n * sizeof(int));
+  float* qbuf = scratch;
+  int* flags = reinterpret_cast<int*>(scratch + (size_t)n * kP2Rows);
+  cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), s);
+  float* A = ws.a.p[0];
+  float* R = ws.a.p[1];
+  float* Q = ws.a.p[2];
+  void* args[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n};
+  const int grid = (n + kPanelW - 1) / kPanelW;
+  if (cudaLaunchCooperativeKernel((const void*)gs_panel2<Bn, V>, dim3(grid), dim3(kPanelThreads), args, 0, s) !=
+      cudaSuccess)
+    launch_failed("GRAMSCHM panel2: cooperative launch rejected");
+}
+
+// PF_GS_PANEL=1 forces the per-column panel kernel (A/B runs).
+inline bool panel_v1_forced() {
+  static const bool f = [] {
+    const char* e = std::getenv("PF_GS_PANEL");
+    return e && e[0] == '1';
+  }();
+  return f;
+}
+
 template <int V>
 struct Run {
   static void run(Workspace& ws, cudaStream_t s) {
@@ -313,6 +512,8 @@ struct Run {
     } else if constexpr (K.vec == 0) {
       cudaGraphExec_t g = cached_graph(ws, V, &s1_sequence<B_GRAMSCHM, V>);
       cudaGraphLaunch(g, s);
+    } else if (m <= kP2Rows && !panel_v1_forced()) {
+      launch_panel2<B_GRAMSCHM, V>(ws, s);
     } else {
       launch_panel<B_GRAMSCHM, V>(ws, s);
     }

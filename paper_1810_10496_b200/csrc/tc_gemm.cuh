@@ -205,6 +205,36 @@ __device__ __forceinline__ void epilogue_rows32(uint32_t taddr, int ncols, int r
   }
 }
 
+// Lane-per-row epilogue (each lane stores 32 consecutive columns of its own
+// row straight from its TMEM registers; no staging, uncoalesced across the
+// warp).  Kept as the A/B alternative to epilogue_rows32 (PF_TC_DIAG bit 16).
+__device__ __forceinline__ void epilogue_lane_rows(uint32_t taddr, int ncols, int row0, int col0, int M, int N,
+                                                   float alpha, float beta, const float* Cin, int ldc, float* D,
+                                                   int ldd, bool split, int lane) {
+  const int row = row0 + lane;
+#pragma unroll 1
+  for (int c = 0; c < ncols / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + (uint32_t)(c * 32), r);
+    const int cb = col0 + c * 32;
+    if (row < M) {
+      float* drow = D + (size_t)row * ldd;
+      const float* crow = Cin + (size_t)row * ldc;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = cb + j;
+        if (col < N) {
+          const float v = alpha * __uint_as_float(r[j]);
+          if (split)
+            atomicAdd(drow + col, v);
+          else
+            drow[col] = beta != 0.f ? fmaf(beta, crow[col], v) : v;
+        }
+      }
+    }
+  }
+}
+
 }  // namespace tc
 
 // Pack op(X) (R x K logical, rows = M for A / N for B) into hi/lo K-major

@@ -43,6 +43,9 @@ constexpr int kTmaThreads = 192;
 
 struct TmaParams {
   CUtensorMap ta, tb, ta2, tb2;  // 2nd pair: K-concatenated product (SYR2K)
+  CUtensorMap tc, td;            // epilogue: Cin / D as 32x32 SWIZZLE_128B boxes (valid iff tma_epi)
+  int tma_epi;
+  int creduce;                   // split-K partials reduced across the z-cluster through DSMEM (tc_tma_kernel)
   int kblocks, kb_per_split, kb1;
   int a_mn, b_mn;                // operand is MN-major (contiguous along M / N)
   int M, N;
@@ -54,7 +57,7 @@ struct TmaParams {
   int upper_only;
   uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides / k-step advance (bytes)
   int idesc_override;                 // probe only: -1 auto, else (a_major | b_major << 1)
-  int diag;                           // diagnostics only (PF_TC_DIAG): 1 skip lo split, 2 skip MMAs, 4 skip loads, 8 skip epilogue
+  int diag;                           // diagnostics only (PF_TC_DIAG): 1 skip lo split, 2 skip MMAs, 4 skip loads, 8 skip epilogue, 16 lane-row epilogue, 32 smem-transpose epilogue
 };
 
 namespace tma {
@@ -98,12 +101,163 @@ __device__ __forceinline__ uint32_t idesc(int m, int n, int a_mn, int b_mn) {
 
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+__device__ __forceinline__ void reduce_add_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// Epilogue of one warp through TMA (the tile rows row0 .. row0+31 = TMEM
+// lanes, ncols accumulator columns from col0).  The warp's Cin boxes (32x32,
+// SWIZZLE_128B) are requested with one mbarrier before the first TMEM read;
+// each 32-column chunk is combined in place -- lane = row, float4 chunk j at
+// 16 * (j ^ (row % 8)), conflict-free -- and written back by one TMA store
+// (or a TMA add-reduction onto the beta-prescaled D for split-K).  buf:
+// 1024-byte aligned, ncols / 32 * 4 KB; bar: this warp's mbarrier (phase 0).
+__device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr, int ncols, int row0, int col0,
+                                             bool split, uint8_t* buf, uint32_t bar, int lane) {
+  if (row0 >= p.M) return;  // warp-uniform
+  const int nch = min(ncols / 32, (p.N - col0 + 31) / 32);
+  const bool use_c = !split && p.beta != 0.f;
+  const uint32_t sbuf = tc::smem_u32(buf);
+  if (use_c && lane == 0) {
+    tc::mbar_expect_tx(bar, (uint32_t)nch * 4096u);
+    for (int c = 0; c < nch; ++c) load_2d(sbuf + c * 4096, &p.tc, col0 + c * 32, row0, bar);
+  }
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    uint32_t r[32];
+    tc::tmem_ld32(taddr + (uint32_t)(c * 32), r);
+    if (use_c && c == 0) tc::mbar_wait(bar, 0);
+    float4* row = reinterpret_cast<float4*>(buf + c * 4096 + lane * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4* slot = row + (j ^ (lane & 7));
+      float4 v = make_float4(p.alpha * __uint_as_float(r[4 * j]), p.alpha * __uint_as_float(r[4 * j + 1]),
+                             p.alpha * __uint_as_float(r[4 * j + 2]), p.alpha * __uint_as_float(r[4 * j + 3]));
+      if (use_c) {
+        const float4 ci = *slot;
+        v = make_float4(fmaf(p.beta, ci.x, v.x), fmaf(p.beta, ci.y, v.y), fmaf(p.beta, ci.z, v.z),
+                        fmaf(p.beta, ci.w, v.w));
+      }
+      *slot = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      if (split)
+        reduce_add_2d(&p.td, sbuf + c * 4096, col0 + c * 32, row0);
+      else
+        store_2d(&p.td, sbuf + c * 4096, col0 + c * 32, row0);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+}
+
+// ---- split-K reduction across a z-cluster (GEMM-sized problems: one launch,
+// no beta pre-pass, no atomics).  Partials are staged row-major 128 x 128
+// fp32 (512-byte rows) with the 16-byte chunk index XORed by row % 8, so the
+// lane-per-row TMEM stores and the row-contiguous reads are conflict-free.
+__device__ __forceinline__ uint32_t partial_off(int row, int chunk) {
+  return (uint32_t)row * 512u + (uint32_t)((chunk ^ (row & 7)) * 16);
+}
+
+__device__ __forceinline__ void stage_partial(uint32_t taddr, uint8_t* buf, int row) {
+  const uint32_t sbuf = tc::smem_u32(buf);
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[32];
+    tc::tmem_ld32(taddr + (uint32_t)(c * 32), r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      sts128(sbuf + partial_off(row, c * 8 + j),
+             make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                         __uint_as_float(r[4 * j + 3])));
+  }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float4 ld_dsmem128(uint32_t cluster_addr) {
+  float4 v;
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(cluster_addr)
+      : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void reduce_partials(const TmaParams& p, uint8_t* buf, int m0, int n0, int S, int rank) {
+  const uint32_t sbuf = tc::smem_u32(buf);
+  const int r0 = 128 * rank / S, r1 = 128 * (rank + 1) / S;
+  const int items = (r1 - r0) * 32;  // float4 chunks of this CTA's rows
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int row = r0 + it / 32, chunk = it % 32;
+    const int grow = m0 + row, gcol = n0 + 4 * chunk;
+    if (grow >= p.M || gcol >= p.N) continue;
+    const uint32_t off = partial_off(row, chunk);
+    // all S remote loads in flight before the (fixed-order, reproducible) sum
+    float4 part[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < S) {
+        uint32_t peer;
+        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(sbuf + off), "r"(q));
+        part[q] = ld_dsmem128(peer);
+      }
+    }
+    float4 acc = part[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) {
+      if (q < S) {
+        acc.x += part[q].x;
+        acc.y += part[q].y;
+        acc.z += part[q].z;
+        acc.w += part[q].w;
+      }
+    }
+    float o[4] = {p.alpha * acc.x, p.alpha * acc.y, p.alpha * acc.z, p.alpha * acc.w};
+    const float* crow = p.Cin + (size_t)grow * p.ldc;
+    float* drow = p.D + (size_t)grow * p.ldd;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (gcol + e < p.N) {
+        if (p.beta != 0.f) o[e] = fmaf(p.beta, crow[gcol + e], o[e]);
+        drow[gcol + e] = o[e];
+      }
+    }
+  }
+}
+
 }  // namespace tma
 
 template <BenchId Bn, int V>
 __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_constant__ TmaParams p) {
   extern __shared__ uint8_t tma_smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar;
+  __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar, epi_bar[4];
   __shared__ uint32_t tmem_slot;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -112,7 +266,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
   const int m0 = mb * 128, n0 = nb * 128;
   const int kb0 = blockIdx.z * p.kb_per_split;
   const int nkb = min(p.kblocks - kb0, p.kb_per_split);
-  const bool split = gridDim.z > 1;
+  const bool split = gridDim.z > 1 && !p.creduce;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
@@ -121,6 +275,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
     }
     tc::mbar_init(tc::smem_u32(&accum_bar), 1);
+    for (int q = 0; q < 4; ++q) tc::mbar_init(tc::smem_u32(&epi_bar[q]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tma::prefetch_map(&p.ta);
@@ -203,13 +358,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       const int s = i % kTmaStages;
       const uint32_t ph = (i / kTmaStages) & 1;
       tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
-      const float4* raw = reinterpret_cast<const float4*>(smem + (size_t)s * kTmaStageBytes);
-      float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * kTmaStageBytes + 2 * kTmaTileBytes);
+      const uint32_t raw = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
+      const uint32_t lo = raw + 2 * kTmaTileBytes;
 #pragma unroll 4
       for (int q = ct; q < ((p.diag & 1) ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
-        const float4 v = raw[q];
-        lo[q] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y), v.z - tma::trunc_tf32(v.z),
-                            v.w - tma::trunc_tf32(v.w));
+        const float4 v = tma::lds128(raw + 16u * q);
+        tma::sts128(lo + 16u * q, make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
+                                              v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w)));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -220,9 +375,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
     tc::mbar_wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
     const int quad = warp & 3;
-    if (!(p.diag & 8))
+    if (p.creduce)
+      tma::stage_partial(tmem + ((uint32_t)(quad * 32) << 16), smem, quad * 32 + lane);
+    else if (p.tma_epi && !(p.diag & (8 | 16 | 32)))
+      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, split,
+                        smem + (size_t)quad * 32768, tc::smem_u32(&epi_bar[quad]), lane);
+    else if (p.diag & 16)
+      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+                             p.Cin, p.ldc, p.D, p.ldd, split, lane);
+    else if (!(p.diag & 8))
       tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                           p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
+  }
+  if (p.creduce) {
+    // every CTA of the z-cluster holds a 128x128 partial in its ring; CTA r
+    // sums rows [r*128/S, (r+1)*128/S) over all S partials (DSMEM reads)
+    tma::cluster_sync_all();
+    tma::reduce_partials(p, smem, m0, n0, (int)gridDim.z, (int)blockIdx.z);
+    tma::cluster_sync_all();  // peers stop reading this CTA's ring
   }
   tc::fence_before();
   __syncthreads();
@@ -310,7 +480,7 @@ template <BenchId Bn, int V>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
     tc_tma2_kernel(const __grid_constant__ TmaParams p) {
   extern __shared__ uint8_t tma_smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar;
+  __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar, epi_bar[4];
   __shared__ uint32_t tmem_slot;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -331,6 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       tc::mbar_init(tc::smem_u32(&empty_bar[s]), 1);
     }
     tc::mbar_init(tc::smem_u32(&accum_bar), 1);
+    for (int q = 0; q < 4; ++q) tc::mbar_init(tc::smem_u32(&epi_bar[q]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tma::prefetch_map(&p.ta);
@@ -411,13 +582,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       const int s = i % kTmaStages;
       const uint32_t ph = (i / kTmaStages) & 1;
       tc2::wait(tc::smem_u32(&full_bar[s]), ph);
-      const float4* raw = reinterpret_cast<const float4*>(smem + (size_t)s * kTmaStageBytes);
-      float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * kTmaStageBytes + 2 * kTmaTileBytes);
+      const uint32_t raw = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
+      const uint32_t lo = raw + 2 * kTmaTileBytes;
 #pragma unroll 4
       for (int q = ct; q < ((p.diag & 1) ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
-        const float4 v = raw[q];
-        lo[q] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y), v.z - tma::trunc_tf32(v.z),
-                            v.w - tma::trunc_tf32(v.w));
+        const float4 v = tma::lds128(raw + 16u * q);
+        tma::sts128(lo + 16u * q, make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
+                                              v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w)));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -428,7 +599,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
     tc2::wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
     const int quad = warp & 3;
-    if (!(p.diag & 8))
+    if (p.tma_epi && !(p.diag & (8 | 16 | 32)))
+      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, split,
+                        smem + (size_t)quad * 32768, tc::smem_u32(&epi_bar[quad]), lane);
+    else if (p.diag & 16)
+      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+                             p.Cin, p.ldc, p.D, p.ldd, split, lane);
+    else if (!(p.diag & 8))
       tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                           p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
   }
@@ -518,12 +695,36 @@ inline bool tc_pair_ok(int64_t m, int64_t n) {
   return enabled && m >= 256 && n >= 256;
 }
 
-// split-K factor: fill ~148 SMs when the output has too few tiles
-inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair) {
-  const int64_t ctas = pair ? 2 * ((m + 255) / 256) * ((n + 255) / 256) : ((m + 127) / 128) * ((n + 127) / 128);
+// split-K factor: fill ~148 SMs when the output has too few (active) tiles;
+// upper: only tiles on or above the block diagonal run (CORR/COVAR Gram)
+inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair, bool upper = false) {
+  const int64_t bm = pair ? (m + 255) / 256 : (m + 127) / 128, bn = pair ? (n + 255) / 256 : (n + 127) / 128;
+  int64_t tiles = bm * bn;
+  if (upper) {
+    tiles = 0;
+    for (int64_t i = 0; i < bm; ++i) tiles += std::max<int64_t>(0, bn - i);
+  }
+  const int64_t ctas = pair ? 2 * tiles : tiles;
   int splits = 1;
   if (ctas < 74) splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / ctas, kblocks / 2));
   const int per = (kblocks + splits - 1) / splits;
+  return (kblocks + per - 1) / per;
+}
+
+// z-cluster size for split-K with an in-cluster reduction: 128x128 tiles,
+// up to 8 (portable cluster limit) k-splits of >= 1 k block when the output
+// alone would leave more than half the SMs idle; 1 = no cluster split.
+inline int tc_cluster_splits(int64_t m, int64_t n, int kblocks) {
+  static const bool enabled = [] {  // opt-in (PF_TC_CREDUCE=1): slower than the TMA add-reduction on B200
+    const char* e = std::getenv("PF_TC_CREDUCE");
+    return e && e[0] == '1';
+  }();
+  if (!enabled) return 1;
+  const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  if (tiles >= 74 || kblocks < 2) return 1;
+  int z = (int)std::min<int64_t>(8, std::max<int64_t>(1, 148 / tiles));
+  z = std::min(z, kblocks);
+  const int per = (kblocks + z - 1) / z;
   return (kblocks + per - 1) / per;
 }
 
@@ -551,12 +752,30 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
     p.ta2 = p.ta;
     p.tb2 = p.tb;
   }
+  // TMA epilogue when D (and Cin, if read) are 16-byte aligned with 16-byte pitches
+  p.tma_epi = (reinterpret_cast<uintptr_t>(a.D) % 16 == 0 && (a.ldd * 4) % 16 == 0 &&
+               tma::make_map(&p.td, a.D, a.N, a.M, a.ldd, 32, 32, false))
+                  ? 1
+                  : 0;
+  if (p.tma_epi && a.beta != 0.f)
+    p.tma_epi = (a.Cin && reinterpret_cast<uintptr_t>(a.Cin) % 16 == 0 && (a.ldc * 4) % 16 == 0 &&
+                 tma::make_map(&p.tc, a.Cin, a.N, a.M, a.ldc, 32, 32, false))
+                    ? 1
+                    : 0;
   const int kb1 = (a.K + 31) / 32;
   const int kblocks = a.A2 ? 2 * kb1 : kb1;
-  const bool pair = tc_pair_ok(a.M, a.N);
-  const int zs = tc_tma_splits(a.M, a.N, kblocks, pair);
+  // split-K problems: beta pre-pass + TMA add-reductions (PF_TC_CREDUCE=1:
+  // reduce the partials inside a z-cluster of single-CTA tiles instead)
+  const int cz = tc_cluster_splits(a.M, a.N, kblocks);
+  p.creduce = cz > 1 ? 1 : 0;
+  // CTA pairs only for problems that fill the GPU without split-K (GEMM 512^3:
+  // 128 single-CTA split-K tiles beat 64 split-K pair halves)
+  const bool up = a.upper_only != 0;
+  const bool pair = !p.creduce && tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
+  const int zs = p.creduce ? cz : tc_tma_splits(a.M, a.N, kblocks, pair, up);
   const int per = (kblocks + zs - 1) / zs;
-  if (zs > 1) tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
+  if (zs > 1 && !p.creduce)
+    tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
   p.kblocks = kblocks;
   p.kb_per_split = per;
   p.kb1 = kb1;
@@ -575,7 +794,22 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(tc_tma2_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     configured = true;
   }
-  if (pair)
+  if (p.creduce) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs);
+    cfg.blockDim = dim3(kTmaThreads);
+    cfg.dynamicSmemBytes = kTmaSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = (unsigned)zs;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc_tma_kernel<Bn, V>, p) != cudaSuccess)
+      launch_failed("tcgen05 split-K cluster launch rejected");
+  } else if (pair)
     tc_tma2_kernel<Bn, V><<<dim3(2 * cdiv(a.N, 256), cdiv(a.M, 256), zs), kTmaThreads, kTmaSmem, s>>>(p);
   else
     tc_tma_kernel<Bn, V><<<dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs), kTmaThreads, kTmaSmem, s>>>(p);
@@ -583,9 +817,11 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
 }
 
 // launches of one TMA-path product: [prescale] + gemm
-inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false) {
+inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false, bool upper = false) {
   const int kblocks = (int)((dual ? 2 : 1) * ((k + 31) / 32));
-  return tc_tma_splits(m, n, kblocks, tc_pair_ok(m, n)) > 1 ? 2 : 1;
+  if (tc_cluster_splits(m, n, kblocks) > 1) return 1;
+  const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, upper) <= 2;
+  return tc_tma_splits(m, n, kblocks, pair, upper) > 1 ? 2 : 1;
 }
 
 }  // namespace pf
