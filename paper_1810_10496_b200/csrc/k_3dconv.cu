@@ -417,13 +417,14 @@ struct Run {
     } else {
       switch (c3_mode()) {
         case -1: launch_s2<V>(A, B, ni, nj, nk, s); break;
-        case 1: launch_s2d<V, 4, 2, 32, 64, 1, 1>(A, B, ni, nj, nk, s); break;
+        case 1: launch_s2d<V, 2, 2, 4, 64, 2, 1>(A, B, ni, nj, nk, s); break;
         case 2: launch_s2d<V, 2, 2, 32, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        case 3: launch_s2d<V, 2, 3, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        case 4: launch_s2d<V, 4, 2, 16, 64, 1, 1>(A, B, ni, nj, nk, s); break;
-        case 5: launch_s2d<V, 2, 2, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        case 6: launch_s2d<V, 3, 2, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        default: launch_s2d<V, 2, 2, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        case 3: launch_s2d<V, 2, 1, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        case 4: launch_s2d<V, 1, 2, 8, 64, 4, 1>(A, B, ni, nj, nk, s); break;
+        case 5: launch_s2d<V, 2, 2, 8, 32, 4, 1>(A, B, ni, nj, nk, s); break;
+        case 6: launch_s2d<V, 2, 3, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        case 7: launch_s2d<V, 2, 2, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
+        default: launch_s2d<V, 2, 2, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
       }
     }
   }

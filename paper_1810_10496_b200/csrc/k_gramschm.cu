@@ -326,10 +326,10 @@ template <BenchId Bn, int V>
 __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict__ A, float* __restrict__ R,
                                                               float* __restrict__ Q, float* __restrict__ qbuf,
                                                               int* __restrict__ flags, int m, int n) {
-  __shared__ __align__(16) float qs[2][kP2Rows];
+  extern __shared__ __align__(16) float qpan[];  // [16][2048]: a panel's q vectors
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int b = blockIdx.x, c0 = b * kPanelW, w = min(kPanelW, n - c0);
-  float* st = &qs[0][0];  // staging for the panel load / store: 128 rows x 17
+  float* st = qpan;  // staging for the panel load / store: 128 rows x 17
   float a[2][64];
 
   // ---- load the panel (coalesced 16-float row segments through shared memory)
@@ -350,25 +350,26 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   __syncthreads();
 
   int step = 0;
-  // ---- apply earlier panels
+  // ---- apply earlier panels: the whole panel's 16 q vectors (128 KB) are
+  // copied into shared memory with cp.async behind one flag acquire, then
+  // every warp applies them back to back with no further block barriers
   for (int pb = 0; pb < b; ++pb) {
     if (t == 0)
       while (ld_acquire(flags + pb) == 0) {
       }
+    __syncthreads();  // also: every warp is done with the previous panel's q
+    const float4* src = reinterpret_cast<const float4*>(qbuf + (size_t)pb * kPanelW * kP2Rows);
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(qpan));
+#pragma unroll 8
+    for (int e = 0; e < kPanelW * kP2Rows / 4 / kPanelThreads; ++e) {
+      const int idx = t + kPanelThreads * e;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * idx), "l"(src + idx) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    const float* qp = qbuf + (size_t)pb * kPanelW * kP2Rows;
-    float4 pre0 = __ldcg(reinterpret_cast<const float4*>(qp) + t);
-    float4 pre1 = __ldcg(reinterpret_cast<const float4*>(qp) + 256 + t);
-    for (int kk = 0; kk < kPanelW; ++kk, ++step) {
+    for (int kk = 0; kk < kPanelW; ++kk) {
       const int k = pb * kPanelW + kk;
-      float* qb = qs[step & 1];
-      reinterpret_cast<float4*>(qb)[t] = pre0;
-      reinterpret_cast<float4*>(qb)[256 + t] = pre1;
-      if (kk + 1 < kPanelW) {
-        pre0 = __ldcg(reinterpret_cast<const float4*>(qp + (size_t)(kk + 1) * kP2Rows) + t);
-        pre1 = __ldcg(reinterpret_cast<const float4*>(qp + (size_t)(kk + 1) * kP2Rows) + 256 + t);
-      }
-      __syncthreads();
+      const float* qb = qpan + kk * kP2Rows;
       float q[64];
 #pragma unroll
       for (int g = 0; g < 16; ++g) {
@@ -388,12 +389,13 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
       }
     }
   }
+  __syncthreads();  // qpan is reused by the factorisation below
 
   // ---- factor the own panel
   float rdiag[2] = {1.f, 1.f};  // 1 / R[k][k] of the two own columns
   for (int kk = 0; kk < w; ++kk, ++step) {
     const int k = c0 + kk;
-    float* qb = qs[step & 1];
+    float* qb = qpan + (step & 1) * kP2Rows;
     if (warp == kk / 2) {
       // the pivot column's register slice is selected by a compile-time index
       // (a runtime a[kk & 1] would demote the whole panel to local memory)
@@ -479,7 +481,13 @@ void launch_panel2(Workspace& ws, cudaStream_t s) {
   float* Q = ws.a.p[2];
   void* args[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n};
   const int grid = (n + kPanelW - 1) / kPanelW;
-  if (cudaLaunchCooperativeKernel((const void*)gs_panel2<Bn, V>, dim3(grid), dim3(kPanelThreads), args, 0, s) !=
+  constexpr size_t smem = (size_t)kPanelW * kP2Rows * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gs_panel2<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  if (cudaLaunchCooperativeKernel((const void*)gs_panel2<Bn, V>, dim3(grid), dim3(kPanelThreads), args, smem, s) !=
       cudaSuccess)
     launch_failed("GRAMSCHM panel2: cooperative launch rejected");
 }

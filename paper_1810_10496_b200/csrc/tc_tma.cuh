@@ -774,8 +774,12 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
   const bool pair = !p.creduce && tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
   const int zs = p.creduce ? cz : tc_tma_splits(a.M, a.N, kblocks, pair, up);
   const int per = (kblocks + zs - 1) / zs;
-  if (zs > 1 && !p.creduce)
-    tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
+  if (zs > 1 && !p.creduce) {
+    if (a.beta == 0.f)
+      cudaMemset2DAsync(a.D, (size_t)a.ldd * sizeof(float), 0, (size_t)a.N * sizeof(float), a.M, s);
+    else
+      tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
+  }
   p.kblocks = kblocks;
   p.kb_per_split = per;
   p.kb1 = kb1;
