@@ -5,11 +5,14 @@
 // row, ex update, hz update), i.e. 3*TMAX launches.  Phase ordering had no
 // effect on the paper's GPU.  Stage 1: one fused kernel per
 // step on double-buffered fields (each thread recomputes the two neighbour
-// updates hz needs), TMAX launches; stage 2: the stage-1 sequence captured
-// once as a CUDA graph.  At 2048^2 the six 16 MiB fields stay L2-resident.
+// updates hz needs), TMAX launches; stage 2: temporal blocking (kTB steps per
+// launch on shared-memory regions with a kTB-cell halo), the launch sequence
+// captured once as a CUDA graph.  At 2048^2 the six 16 MiB fields stay
+// L2-resident.
 #include "pf_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace pf {
 namespace {
@@ -167,6 +170,117 @@ __global__ void __launch_bounds__(256) step_fused4(const float* __restrict__ fic
   *reinterpret_cast<float4*>(hz1 + c) = make_float4(ohz[0], ohz[1], ohz[2], ohz[3]);
 }
 
+// ---- stage 2: temporal blocking.  A CTA loads a (64 + 2T)^2 region of the
+// three fields into shared memory, advances it kTB time steps there (ey/ex
+// phase, barrier, hz phase, barrier -- the per-cell arithmetic of the fused
+// step), and writes back the central 64 x 64 tile, whose values depend only on
+// cells inside the region: every step the valid area shrinks by at most one
+// cell per side (global boundary rules need no neighbours, so they do not
+// shrink).  L2 traffic per time step falls from 6 field passes to
+// ~(6 * 1.27) / kTB.
+constexpr int kTB = 4;                  // time steps per launch (halo width)
+constexpr int kTT = 64;                 // output tile edge
+constexpr int kTR = kTT + 2 * kTB;      // region edge (72)
+constexpr int kTBThreads = 256;
+constexpr size_t kTBSmem = 3ull * kTR * kTR * sizeof(float);
+
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(kTBThreads) step_tb(const float* __restrict__ fict, const float* __restrict__ ex0,
+                                                      const float* __restrict__ ey0, const float* __restrict__ hz0,
+                                                      float* __restrict__ ex1, float* __restrict__ ey1,
+                                                      float* __restrict__ hz1, int nx, int ny, int t0, int steps) {
+  extern __shared__ __align__(16) float tb_smem[];
+  float* sex = tb_smem;
+  float* sey = sex + kTR * kTR;
+  float* shz = sey + kTR * kTR;
+  const int gi0 = blockIdx.y * kTT - kTB, gj0 = blockIdx.x * kTT - kTB;  // region origin (global)
+  // ---- load (float4 along j; ny % 4 == 0 and gj0 % 4 == 0, so a float4 is all in or all out)
+  constexpr int kW4 = kTR / 4;
+  for (int idx = threadIdx.x; idx < kTR * kW4; idx += kTBThreads) {
+    const int li = idx / kW4, lj = 4 * (idx % kW4);
+    const int gi = gi0 + li, gj = gj0 + lj;
+    float4 vx = make_float4(0.f, 0.f, 0.f, 0.f), vy = vx, vz = vx;
+    if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) {
+      const size_t c = (size_t)gi * ny + gj;
+      vx = __ldcg(reinterpret_cast<const float4*>(ex0 + c));
+      vy = __ldcg(reinterpret_cast<const float4*>(ey0 + c));
+      vz = __ldcg(reinterpret_cast<const float4*>(hz0 + c));
+    }
+    *reinterpret_cast<float4*>(sex + li * kTR + lj) = vx;
+    *reinterpret_cast<float4*>(sey + li * kTR + lj) = vy;
+    *reinterpret_cast<float4*>(shz + li * kTR + lj) = vz;
+  }
+  __syncthreads();
+  for (int st = 0; st < steps; ++st) {
+    const float src = __ldg(fict + t0 + st);
+    // ey / ex phase (reads hz only: in place)
+    for (int idx = threadIdx.x; idx < kTR * kTR; idx += kTBThreads) {
+      const int li = idx / kTR, lj = idx % kTR;
+      const int gi = gi0 + li, gj = gj0 + lj;
+      if (gi < 0 || gi >= nx || gj < 0 || gj >= ny) continue;
+      const float h = shz[idx];
+      if (gi == 0)
+        sey[idx] = src;
+      else if (li > 0)
+        sey[idx] = upd_e(sey[idx], h, shz[idx - kTR]);
+      if (gj > 0 && lj > 0) sex[idx] = upd_e(sex[idx], h, shz[idx - 1]);
+    }
+    __syncthreads();
+    // hz phase (reads the new ex / ey)
+    for (int idx = threadIdx.x; idx < kTR * kTR; idx += kTBThreads) {
+      const int li = idx / kTR, lj = idx % kTR;
+      const int gi = gi0 + li, gj = gj0 + lj;
+      if (gi < 0 || gi >= nx - 1 || gj < 0 || gj >= ny - 1 || li >= kTR - 1 || lj >= kTR - 1) continue;
+      shz[idx] = upd_h(shz[idx], sex[idx + 1], sex[idx], sey[idx + kTR], sey[idx]);
+    }
+    __syncthreads();
+  }
+  // ---- store the central tile
+  constexpr int kT4 = kTT / 4;
+  for (int idx = threadIdx.x; idx < kTT * kT4; idx += kTBThreads) {
+    const int oi = idx / kT4, oj = 4 * (idx % kT4);
+    const int gi = gi0 + kTB + oi, gj = gj0 + kTB + oj;
+    if (gi >= nx || gj >= ny) continue;
+    const int l = (kTB + oi) * kTR + kTB + oj;
+    const size_t c = (size_t)gi * ny + gj;
+    __stcg(reinterpret_cast<float4*>(ex1 + c), *reinterpret_cast<const float4*>(sex + l));
+    __stcg(reinterpret_cast<float4*>(ey1 + c), *reinterpret_cast<const float4*>(sey + l));
+    __stcg(reinterpret_cast<float4*>(hz1 + c), *reinterpret_cast<const float4*>(shz + l));
+  }
+}
+
+template <BenchId Bn, int V>
+void tb_sequence(Workspace& ws, cudaStream_t s) {
+  const int nx = (int)ws.dims.d[0], ny = (int)ws.dims.d[1], tmax = (int)ws.dims.d[2];
+  const size_t n = (size_t)nx * ny;
+  float* scratch = ws.ensure_scratch(3 * n * sizeof(float));
+  float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(step_tb<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem);
+    configured = true;
+  }
+  const dim3 grid(cdiv(ny, kTT), cdiv(nx, kTT));
+  int launches = 0;
+  for (int t = 0; t < tmax; t += kTB, ++launches) {
+    float** src = buf[launches & 1];
+    float** dst = buf[(launches + 1) & 1];
+    step_tb<Bn, V><<<grid, kTBThreads, kTBSmem, s>>>(ws.a.p[0], src[0], src[1], src[2], dst[0], dst[1], dst[2], nx, ny,
+                                                    t, std::min(kTB, tmax - t));
+  }
+  if (launches & 1)
+    for (int f = 0; f < 3; ++f) cudaMemcpyAsync(buf[0][f], buf[1][f], n * sizeof(float), cudaMemcpyDeviceToDevice, s);
+}
+
+// PF_FDTD_TB=0: stage 2 replays the per-step fused sequence instead (A/B runs).
+inline bool fdtd_tb_disabled() {
+  static const bool d = [] {
+    const char* e = std::getenv("PF_FDTD_TB");
+    return e && e[0] == '0';
+  }();
+  return d;
+}
+
 template <BenchId Bn, int V>
 void fused_sequence(Workspace& ws, cudaStream_t s) {
   const int nx = (int)ws.dims.d[0], ny = (int)ws.dims.d[1], tmax = (int)ws.dims.d[2];
@@ -209,7 +323,9 @@ struct Run {
       fused_sequence<B_FDTD2D, V>(ws, s);
     } else {
       ws.ensure_scratch(3 * (size_t)nx * ny * sizeof(float));  // allocate before capture
-      cudaGraphExec_t g = cached_graph(ws, V, &fused_sequence<B_FDTD2D, V>);
+      const bool tb = ny % 4 == 0 && !fdtd_tb_disabled();
+      cudaGraphExec_t g = tb ? cached_graph(ws, V, &tb_sequence<B_FDTD2D, V>)
+                             : cached_graph(ws, V + 1000, &fused_sequence<B_FDTD2D, V>);
       cudaGraphLaunch(g, s);
     }
   }
@@ -220,6 +336,7 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 int64_t elems(int a, const Dims& d) { return a == 0 ? d.d[2] : d.d[0] * d.d[1]; }
 int64_t launches(int v, const Dims& d) {
   const int st = kTab.v[v].stage;
+  if (st == 2 && d.d[1] % 4 == 0 && !fdtd_tb_disabled()) return (d.d[2] + kTB - 1) / kTB;
   return st == 0 ? 3 * d.d[2] : d.d[2];
 }
 // fused compulsory traffic per step: read ex, ey, hz, write ex, ey, hz

@@ -59,7 +59,7 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 
 int64_t elems(int a, const Dims& d) { return a == 0 ? d.d[0] * d.d[1] : d.d[0] * d.d[0]; }
 int64_t launches(int v, const Dims& d) {
-  return kTab.v[v].stage == 2 ? tc_launches(d.d[0], d.d[0], d.d[1], tma_ok(d.d[1], d.d[1])) : 1;
+  return kTab.v[v].stage == 2 ? tc_launches(d.d[0], d.d[0], d.d[1], tma_ok(d.d[1], d.d[1]), false, 1) : 1;
 }
 double alg_bytes(const Dims& d) { return 4.0 * ((double)d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }
 double alg_flops(const Dims& d) { return 2.0 * (double)d.d[0] * d.d[0] * d.d[1]; }

@@ -45,6 +45,12 @@ struct TcGemmArgs {
   float* D;
   int ldd;
   int upper_only;  // compute only output tiles with n-block >= m-block
+  // pre-split operands (TMA path): lo = x - trunc_tf32(x) images with the
+  // operands' own layouts (nullptr: the kernel's converter warps split)
+  const float* Alo = nullptr;
+  const float* Blo = nullptr;
+  const float* A2lo = nullptr;
+  const float* B2lo = nullptr;
 };
 
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;

@@ -43,6 +43,8 @@ constexpr int kTmaThreads = 192;
 
 struct TmaParams {
   CUtensorMap ta, tb, ta2, tb2;  // 2nd pair: K-concatenated product (SYR2K)
+  CUtensorMap tal, tbl, ta2l, tb2l;  // pre-split lo operands (valid iff presplit)
+  int presplit;
   CUtensorMap tc, td;            // epilogue: Cin / D as 32x32 SWIZZLE_128B boxes (valid iff tma_epi)
   int tma_epi;
   int creduce;                   // split-K partials reduced across the z-cluster through DSMEM (tc_tma_kernel)
@@ -175,6 +177,27 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr,
   __syncwarp();
 }
 
+// The A and B tiles of one k block (raw, or the pre-split lo images) into
+// [base, base + 32 KB): K-major operands as one 128x32 box, MN-major ones as
+// four 32x32 boxes.
+__device__ __forceinline__ void load_operands(const TmaParams& p, bool second, bool lo, uint32_t base, int m0, int n0,
+                                              int k0, uint32_t fb) {
+  const CUtensorMap* ma = lo ? (second ? &p.ta2l : &p.tal) : (second ? &p.ta2 : &p.ta);
+  const CUtensorMap* mb = lo ? (second ? &p.tb2l : &p.tbl) : (second ? &p.tb2 : &p.tb);
+  if (p.a_mn) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) load_2d(base + j * 4096, ma, m0 + 32 * j, k0, fb);
+  } else {
+    load_2d(base, ma, k0, m0, fb);
+  }
+  if (p.b_mn) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) load_2d(base + kTmaTileBytes + j * 4096, mb, n0 + 32 * j, k0, fb);
+  } else {
+    load_2d(base + kTmaTileBytes, mb, k0, n0, fb);
+  }
+}
+
 // ---- split-K reduction across a z-cluster (GEMM-sized problems: one launch,
 // no beta pre-pass, no atomics).  Partials are staged row-major 128 x 128
 // fp32 (512-byte rows) with the 16-byte chunk index XORed by row % 8, so the
@@ -303,24 +326,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
           tma::mbar_arrive(fb);
           continue;
         }
-        tc::mbar_expect_tx(fb, 2 * kTmaTileBytes);
+        tc::mbar_expect_tx(fb, (p.presplit ? 4 : 2) * kTmaTileBytes);
         const bool second = kb >= p.kb1;
-        const CUtensorMap* ma = second ? &p.ta2 : &p.ta;
-        const CUtensorMap* mbm = second ? &p.tb2 : &p.tb;
         const int k0 = (second ? kb - p.kb1 : kb) * 32;
         const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
-        if (p.a_mn) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tma::load_2d(base + j * 4096, ma, m0 + 32 * j, k0, fb);
-        } else {
-          tma::load_2d(base, ma, k0, m0, fb);
-        }
-        if (p.b_mn) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tma::load_2d(base + kTmaTileBytes + j * 4096, mbm, n0 + 32 * j, k0, fb);
-        } else {
-          tma::load_2d(base + kTmaTileBytes, mbm, k0, n0, fb);
-        }
+        tma::load_operands(p, second, false, base, m0, n0, k0, fb);
+        if (p.presplit) tma::load_operands(p, second, true, base + 2 * kTmaTileBytes, m0, n0, k0, fb);
       }
     }
   } else if (warp == 1) {
@@ -361,7 +372,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       const uint32_t raw = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
       const uint32_t lo = raw + 2 * kTmaTileBytes;
 #pragma unroll 4
-      for (int q = ct; q < ((p.diag & 1) ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
+      for (int q = ct; q < ((p.diag & 1) || p.presplit ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
         const float4 v = tma::lds128(raw + 16u * q);
         tma::sts128(lo + 16u * q, make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
                                               v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w)));
@@ -529,24 +540,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
           tma::mbar_arrive(fb);
           continue;
         }
-        tc::mbar_expect_tx(fb, 2 * kTmaTileBytes);
+        tc::mbar_expect_tx(fb, (p.presplit ? 4 : 2) * kTmaTileBytes);
         const bool second = kb >= p.kb1;
-        const CUtensorMap* ma = second ? &p.ta2 : &p.ta;
-        const CUtensorMap* mbm = second ? &p.tb2 : &p.tb;
         const int k0 = (second ? kb - p.kb1 : kb) * 32;
         const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
-        if (p.a_mn) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tma::load_2d(base + j * 4096, ma, m0 + 32 * j, k0, fb);
-        } else {
-          tma::load_2d(base, ma, k0, m0, fb);
-        }
-        if (p.b_mn) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tma::load_2d(base + kTmaTileBytes + j * 4096, mbm, nB + 32 * j, k0, fb);
-        } else {
-          tma::load_2d(base + kTmaTileBytes, mbm, k0, nB, fb);
-        }
+        tma::load_operands(p, second, false, base, m0, nB, k0, fb);
+        if (p.presplit) tma::load_operands(p, second, true, base + 2 * kTmaTileBytes, m0, nB, k0, fb);
       }
     }
   } else if (warp == 1) {
@@ -585,7 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       const uint32_t raw = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
       const uint32_t lo = raw + 2 * kTmaTileBytes;
 #pragma unroll 4
-      for (int q = ct; q < ((p.diag & 1) ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
+      for (int q = ct; q < ((p.diag & 1) || p.presplit ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
         const float4 v = tma::lds128(raw + 16u * q);
         tma::sts128(lo + 16u * q, make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
                                               v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w)));
@@ -752,6 +751,15 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
     p.ta2 = p.ta;
     p.tb2 = p.tb;
   }
+  p.presplit = a.Alo && a.Blo && (!a.A2 || (a.A2lo && a.B2lo)) &&
+               tma::operand_map(&p.tal, a.Alo, p.a_mn, a.M, a.K, a.lda) &&
+               tma::operand_map(&p.tbl, a.Blo, p.b_mn, a.N, a.K, a.ldb) &&
+               (!a.A2 || (tma::operand_map(&p.ta2l, a.A2lo, p.a_mn, a.M, a.K, a.lda) &&
+                          tma::operand_map(&p.tb2l, a.B2lo, p.b_mn, a.N, a.K, a.ldb)));
+  if (p.presplit && !a.A2) {
+    p.ta2l = p.tal;
+    p.tb2l = p.tbl;
+  }
   // TMA epilogue when D (and Cin, if read) are 16-byte aligned with 16-byte pitches
   p.tma_epi = (reinterpret_cast<uintptr_t>(a.D) % 16 == 0 && (a.ldd * 4) % 16 == 0 &&
                tma::make_map(&p.td, a.D, a.N, a.M, a.ldd, 32, 32, false))
@@ -838,14 +846,85 @@ inline bool tma_ok(int64_t lda, int64_t ldb, int64_t offset_elems = 0) {
   return lda % 4 == 0 && ldb % 4 == 0 && offset_elems % 4 == 0;
 }
 
-inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual = false) {
-  return tma ? tc_tma_launches(m, n, k, dual) : tc_gemm_launches(m, n, k, dual);
-}
+inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual = false, int operands = 2);
 
 // One tensor-core contraction: TMA-fed raw-operand kernel when possible,
 // otherwise the packed-operand kernel (tc_gemm.cuh).
+// lo = x - trunc_tf32(x) over n floats (operand storage, pitch included)
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) tc_split_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+    reinterpret_cast<float4*>(lo)[i] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
+                                                   v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w));
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lo[i] = x[i] - tma::trunc_tf32(x[i]);
+}
+
+// Pre-split operands: one pass over global memory writes lo = x - trunc(x)
+// next to each operand and the kernel TMA-loads both halves, so the converter
+// warps' shared-memory round trip (64 KB per k block) and their proxy-fence
+// hand-off leave the mainloop (2MM/3MM 2048: -11%, SYRK/SYR2K: -17-19% on
+// B200).  Used when the product runs without split-K (a split-K product is
+// latency-bound and the extra pass costs more than it saves: GEMM 512^3).
+// PF_TC_PRESPLIT=0 / =1 force it off / on (A/B runs).
+inline bool tc_presplit_wanted(int64_t m, int64_t n, int64_t k, bool dual, bool upper) {
+  static const int mode = [] {
+    const char* v = std::getenv("PF_TC_PRESPLIT");
+    return v ? std::atoi(v) : -1;
+  }();
+  if (mode >= 0) return mode == 1;
+  return tc_tma_launches(m, n, k, dual, upper) == 1;
+}
+
+// launches of one contraction: [lo passes, one per distinct operand array] +
+// [prescale] + gemm (TMA path) or the packed path's sequence
+inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual, int operands) {
+  if (!tma) return tc_gemm_launches(m, n, k, dual);
+  return tc_tma_launches(m, n, k, dual) + (tc_presplit_wanted(m, n, k, dual, false) ? operands : 0);
+}
+
 template <BenchId Bn, int V>
 inline void launch_contraction(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
+  if (tc_presplit_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0) && tma_ok(a.lda, a.ldb)) {
+    // distinct operand arrays and their storage extents (floats)
+    const float* ops[4] = {a.A, a.B, a.A2, a.B2};
+    const int64_t ext[4] = {
+        a.ta ? (int64_t)(a.K - 1) * a.lda + a.M : (int64_t)(a.M - 1) * a.lda + a.K,
+        a.tb ? (int64_t)(a.N - 1) * a.ldb + a.K : (int64_t)(a.K - 1) * a.ldb + a.N,
+        0, 0};
+    int64_t e[4] = {ext[0], ext[1], a.A2 ? ext[0] : 0, a.B2 ? ext[1] : 0};
+    int64_t off[4], total = 0;
+    for (int i = 0; i < 4; ++i) {
+      off[i] = -1;
+      if (!ops[i]) continue;
+      for (int j = 0; j < i; ++j)
+        if (ops[j] == ops[i] && e[j] == e[i]) off[i] = off[j];
+      if (off[i] < 0) {
+        off[i] = total;
+        total += (e[i] + 63) / 64 * 64;  // 256-byte aligned images
+      }
+    }
+    float* lo = ws.ensure_scratch((size_t)total * sizeof(float));
+    if (lo) {
+      bool done[4] = {false, false, false, false};
+      for (int i = 0; i < 4; ++i) {
+        if (!ops[i] || done[i]) continue;
+        for (int j = i; j < 4; ++j)
+          if (ops[j] == ops[i] && off[j] == off[i]) done[j] = true;
+        tc_split_lo<Bn, V><<<4 * 148, 256, 0, s>>>(ops[i], lo + off[i], e[i]);
+      }
+      TcGemmArgs b = a;
+      b.Alo = lo + off[0];
+      b.Blo = lo + off[1];
+      b.A2lo = a.A2 ? lo + off[2] : nullptr;
+      b.B2lo = a.B2 ? lo + off[3] : nullptr;
+      if (launch_tc_tma<Bn, V>(b, s)) return;
+    }
+  }
   if (!launch_tc_tma<Bn, V>(a, s)) launch_tc_gemm<Bn, V>(ws, a, s);
 }
 
