@@ -327,11 +327,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
                                                               float* __restrict__ Q, float* __restrict__ qbuf,
                                                               int* __restrict__ flags, int m, int n) {
   extern __shared__ __align__(16) float qpan[];  // [16][2048]: a panel's q vectors
-  __shared__ volatile int slot_ready[kPanelW];    // own-panel factorisation: slot kk holds q_{c0+kk}
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int b = blockIdx.x, c0 = b * kPanelW, w = min(kPanelW, n - c0);
   float* st = qpan;  // staging for the panel load / store: 128 rows x 17
-  if (t < kPanelW) slot_ready[t] = 0;  // ordered before use by the load loop's barriers
   float a[2][64];
 
   // ---- load the panel (coalesced 16-float row segments through shared memory)
@@ -351,6 +349,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   }
   __syncthreads();
 
+  int step = 0;
   // ---- apply earlier panels: the whole panel's 16 q vectors (128 KB) are
   // copied into shared memory with cp.async behind one flag acquire, then
   // every warp applies them back to back with no further block barriers
@@ -392,56 +391,39 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   }
   __syncthreads();  // qpan is reused by the factorisation below
 
-  // ---- factor the own panel.  q_{c0+kk} goes to its own shared slot kk
-  // (qpan is free again) with a per-slot ready flag, so there is no block
-  // barrier per column: a warp applies q_kk to its columns as soon as slot kk
-  // is flagged, and the owner of column kk+1 updates that column first,
-  // factors it and publishes slot kk+1 before finishing its other column.
-  // Per-column arithmetic and order are unchanged (MGS).
+  // ---- factor the own panel
   float rdiag[2] = {1.f, 1.f};  // 1 / R[k][k] of the two own columns
-  // the pivot column's register slice is selected by a compile-time index
-  // (a runtime a[kk & 1] would demote the whole panel to local memory)
-  auto pivot = [&](float(&col)[64], float& rinv, int kk) {
+  for (int kk = 0; kk < w; ++kk, ++step) {
     const int k = c0 + kk;
-    const float rkk = sqrtf(dot64(col, col));
-    const float inv = 1.0f / rkk;
-    rinv = inv;
-    float* qb = qpan + kk * kP2Rows;
-    float* qg = qbuf + (size_t)k * kP2Rows;
+    float* qb = qpan + (step & 1) * kP2Rows;
+    if (warp == kk / 2) {
+      // the pivot column's register slice is selected by a compile-time index
+      // (a runtime a[kk & 1] would demote the whole panel to local memory)
+      auto pivot = [&](float(&col)[64], float& rinv) {
+        const float rkk = sqrtf(dot64(col, col));
+        const float inv = 1.0f / rkk;
+        rinv = inv;
+        float* qg = qbuf + (size_t)k * kP2Rows;
 #pragma unroll
-    for (int g = 0; g < 16; ++g) {
-      const int row = 128 * g + 4 * lane;
-      float4 v;
-      v.x = row < m ? col[4 * g] * inv : 0.f;
-      v.y = row + 1 < m ? col[4 * g + 1] * inv : 0.f;
-      v.z = row + 2 < m ? col[4 * g + 2] * inv : 0.f;
-      v.w = row + 3 < m ? col[4 * g + 3] * inv : 0.f;
-      reinterpret_cast<float4*>(qb)[32 * g + lane] = v;
-      reinterpret_cast<float4*>(qg)[32 * g + lane] = v;
+        for (int g = 0; g < 16; ++g) {
+          const int row = 128 * g + 4 * lane;
+          float4 v;
+          v.x = row < m ? col[4 * g] * inv : 0.f;
+          v.y = row + 1 < m ? col[4 * g + 1] * inv : 0.f;
+          v.z = row + 2 < m ? col[4 * g + 2] * inv : 0.f;
+          v.w = row + 3 < m ? col[4 * g + 3] * inv : 0.f;
+          reinterpret_cast<float4*>(qb)[32 * g + lane] = v;
+          reinterpret_cast<float4*>(qg)[32 * g + lane] = v;
+        }
+        if (lane == 0) R[(size_t)k * n + k] = rkk;
+      };
+      if (kk & 1)
+        pivot(a[1], rdiag[1]);
+      else
+        pivot(a[0], rdiag[0]);
     }
-    if (lane == 0) R[(size_t)k * n + k] = rkk;
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      slot_ready[kk] = 1;
-    }
-  };
-  auto update = [&](float(&col)[64], const float(&q)[64], int kk, int jj) {
-    const float r = dot64(q, col);
-    if (lane == 0) R[(size_t)(c0 + kk) * n + c0 + jj] = r;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) col[i] = fmaf(-q[i], r, col[i]);
-  };
-  if (warp == 0) pivot(a[0], rdiag[0], 0);
-  const int last_own = 2 * warp < w ? min(2 * warp + 1, w - 1) : 0;  // highest own column
-  for (int kk = 0; kk < last_own; ++kk) {
-    if (lane == 0)
-      while (slot_ready[kk] == 0) {
-      }
-    __syncwarp();
-    __threadfence_block();
+    __syncthreads();
     float q[64];
-    const float* qb = qpan + kk * kP2Rows;
 #pragma unroll
     for (int g = 0; g < 16; ++g) {
       const float4 v = reinterpret_cast<const float4*>(qb)[32 * g + lane];
@@ -450,19 +432,15 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
       q[4 * g + 2] = v.z;
       q[4 * g + 3] = v.w;
     }
-    const int nxt = kk + 1;  // next pivot column
-    const bool mine_next = nxt < w && nxt / 2 == warp;
-    if (mine_next) {  // critical path first
-      if (nxt & 1) {
-        update(a[1], q, kk, nxt);
-        pivot(a[1], rdiag[1], nxt);
-      } else {
-        update(a[0], q, kk, nxt);
-        pivot(a[0], rdiag[0], nxt);
-      }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int jj = 2 * warp + c;
+      if (jj >= w || jj <= kk) continue;
+      float r = dot64(q, a[c]);
+      if (lane == 0) R[(size_t)k * n + c0 + jj] = r;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) a[c][i] = fmaf(-q[i], r, a[c][i]);
     }
-    if (2 * warp < w && 2 * warp > kk && !(mine_next && nxt == 2 * warp)) update(a[0], q, kk, 2 * warp);
-    if (2 * warp + 1 < w && 2 * warp + 1 > kk && !(mine_next && nxt == 2 * warp + 1)) update(a[1], q, kk, 2 * warp + 1);
   }
   // ---- publish the panel's q vectors
   __threadfence();

@@ -147,6 +147,36 @@ def test_tensor_core_tiles_match_oracle(bench, gpu_backend):
     assert not failures, "\n".join(failures)
 
 
+# Config-scale tensor-core paths the small sizes above never reach: CTA-pair
+# tiles without split-K (operands pre-split into lo images, TMA epilogue with
+# beta), pair tiles with a 2-way split (memset pre-pass + TMA add-reductions),
+# the K-concatenated SYR2K product, and CORR's upper-triangle split.
+TC_LARGE_SIZES = {
+    "2MM": [(2048, 2048, 256, 1024)],
+    "SYRK": [(2048, 512)],
+    "SYR2K": [(2048, 256)],
+    "CORR": [(2048, 256)],
+}
+
+
+@pytest.mark.parametrize("bench", [b for b in TC_LARGE_SIZES if b in BUILT])
+def test_tensor_core_config_paths_match_oracle(bench, gpu_backend):
+    from paper_1810_10496_b200.backend import b200
+
+    fam = b200.family(bench)
+    v = next(i for i in range(len(fam.knobs)) if fam.key(i) == "stage=2")
+    failures = []
+    for dims in TC_LARGE_SIZES[bench]:
+        ref = orc.reference(bench, dims, False, gpu_backend.seed, 7)
+        ws = gpu_backend.workspace(bench, dims, False, 7)
+        ws.run(v, samples=1, batch=1, restore=True, flush=False)
+        for k, (g, r) in enumerate(zip(ws.outputs(), ref)):
+            ok, worst = _close(g, r)
+            if not ok:
+                failures.append(f"{dims} out{k}: worst/tol={worst:.3g}")
+    assert not failures, "\n".join(failures)
+
+
 # Stencil tiling edges: partial 128-wide k tiles, j tiles and i runs that end
 # mid-tile, tiny volumes where a run spans several column tiles.
 STENCIL_SIZES = {"3DCONV": [(37, 45, 132), (9, 20, 8), (64, 33, 260)], "2DCONV": [(67, 516), (5, 8)]}
