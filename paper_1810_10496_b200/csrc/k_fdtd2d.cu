@@ -5,10 +5,10 @@
 // row, ex update, hz update), i.e. 3*TMAX launches.  Phase ordering had no
 // effect on the paper's GPU.  Stage 1: one fused kernel per
 // step on double-buffered fields (each thread recomputes the two neighbour
-// updates hz needs), TMAX launches; stage 2: temporal blocking (kTB steps per
-// launch on shared-memory regions with a kTB-cell halo), the launch sequence
-// captured once as a CUDA graph.  At 2048^2 the six 16 MiB fields stay
-// L2-resident.
+// updates hz needs), TMAX launches; stage 2: temporal blocking (4 time steps
+// per launch on 64x64 shared-memory regions with a 4-cell halo), the launch
+// sequence captured once as a CUDA graph.  At 2048^2 the six 16 MiB fields
+// stay L2-resident.
 #include "pf_common.cuh"
 
 #include <algorithm>
@@ -178,26 +178,28 @@ __global__ void __launch_bounds__(256) step_fused4(const float* __restrict__ fic
 // cell per side (global boundary rules need no neighbours, so they do not
 // shrink).  L2 traffic per time step falls from 6 field passes to
 // ~(6 * 1.27) / kTB.
-constexpr int kTB = 4;                  // time steps per launch (halo width)
-constexpr int kTT = 64;                 // output tile edge
-constexpr int kTR = kTT + 2 * kTB;      // region edge (72)
-constexpr int kTBThreads = 256;
+constexpr int kTR = 64;                 // region edge (16 float4 per row)
+constexpr int kTBThreads = 256;         // 4 row-quads per thread per phase
 constexpr size_t kTBSmem = 3ull * kTR * kTR * sizeof(float);
 
-template <BenchId Bn, int V>
+// kTB: time steps per launch = halo width; output tile edge kTR - 2 kTB
+template <BenchId Bn, int V, int kTB>
 __global__ void __launch_bounds__(kTBThreads) step_tb(const float* __restrict__ fict, const float* __restrict__ ex0,
                                                       const float* __restrict__ ey0, const float* __restrict__ hz0,
                                                       float* __restrict__ ex1, float* __restrict__ ey1,
                                                       float* __restrict__ hz1, int nx, int ny, int t0, int steps) {
+  constexpr int kTT = kTR - 2 * kTB;
   extern __shared__ __align__(16) float tb_smem[];
   float* sex = tb_smem;
   float* sey = sex + kTR * kTR;
   float* shz = sey + kTR * kTR;
   const int gi0 = blockIdx.y * kTT - kTB, gj0 = blockIdx.x * kTT - kTB;  // region origin (global)
-  // ---- load (float4 along j; ny % 4 == 0 and gj0 % 4 == 0, so a float4 is all in or all out)
-  constexpr int kW4 = kTR / 4;
-  for (int idx = threadIdx.x; idx < kTR * kW4; idx += kTBThreads) {
-    const int li = idx / kW4, lj = 4 * (idx % kW4);
+  constexpr int kQ = kTR / 4;                                           // float4 per region row
+  constexpr int kItems = kTR * kQ / kTBThreads;                         // 4
+  // ---- load (ny % 4 == 0 and gj0 % 4 == 0: a float4 is all in or all out of the domain)
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int item = threadIdx.x + kTBThreads * r, li = item / kQ, lj = 4 * (item % kQ);
     const int gi = gi0 + li, gj = gj0 + lj;
     float4 vx = make_float4(0.f, 0.f, 0.f, 0.f), vy = vx, vz = vx;
     if (gi >= 0 && gi < nx && gj >= 0 && gj < ny) {
@@ -211,27 +213,57 @@ __global__ void __launch_bounds__(kTBThreads) step_tb(const float* __restrict__ 
     *reinterpret_cast<float4*>(shz + li * kTR + lj) = vz;
   }
   __syncthreads();
+  // Cells outside the domain hold garbage after a step, but no in-domain cell
+  // ever reads them (row 0 takes _fict_, column 0 keeps ex, the last row and
+  // column keep hz), and region-edge garbage moves inward one cell per step.
   for (int st = 0; st < steps; ++st) {
     const float src = __ldg(fict + t0 + st);
     // ey / ex phase (reads hz only: in place)
-    for (int idx = threadIdx.x; idx < kTR * kTR; idx += kTBThreads) {
-      const int li = idx / kTR, lj = idx % kTR;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+      const int item = threadIdx.x + kTBThreads * r, li = item / kQ, lj = 4 * (item % kQ);
       const int gi = gi0 + li, gj = gj0 + lj;
-      if (gi < 0 || gi >= nx || gj < 0 || gj >= ny) continue;
-      const float h = shz[idx];
-      if (gi == 0)
-        sey[idx] = src;
-      else if (li > 0)
-        sey[idx] = upd_e(sey[idx], h, shz[idx - kTR]);
-      if (gj > 0 && lj > 0) sex[idx] = upd_e(sex[idx], h, shz[idx - 1]);
+      const int l = li * kTR + lj;
+      const float4 h = *reinterpret_cast<const float4*>(shz + l);
+      if (li > 0 || gi == 0) {
+        float4 e = *reinterpret_cast<const float4*>(sey + l);
+        if (gi == 0) {
+          e = make_float4(src, src, src, src);
+        } else {
+          const float4 hu = *reinterpret_cast<const float4*>(shz + l - kTR);
+          e = make_float4(upd_e(e.x, h.x, hu.x), upd_e(e.y, h.y, hu.y), upd_e(e.z, h.z, hu.z), upd_e(e.w, h.w, hu.w));
+        }
+        *reinterpret_cast<float4*>(sey + l) = e;
+      }
+      if (lj > 0 || gj > 0) {
+        float4 x = *reinterpret_cast<const float4*>(sex + l);
+        const float hl = lj > 0 ? shz[l - 1] : 0.f;  // lj == 0 < gj: region edge, garbage allowed
+        const float nx0 = gj == 0 ? x.x : upd_e(x.x, h.x, hl);
+        x = make_float4(nx0, upd_e(x.y, h.y, h.x), upd_e(x.z, h.z, h.y), upd_e(x.w, h.w, h.z));
+        *reinterpret_cast<float4*>(sex + l) = x;
+      }
     }
     __syncthreads();
     // hz phase (reads the new ex / ey)
-    for (int idx = threadIdx.x; idx < kTR * kTR; idx += kTBThreads) {
-      const int li = idx / kTR, lj = idx % kTR;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+      const int item = threadIdx.x + kTBThreads * r, li = item / kQ, lj = 4 * (item % kQ);
       const int gi = gi0 + li, gj = gj0 + lj;
-      if (gi < 0 || gi >= nx - 1 || gj < 0 || gj >= ny - 1 || li >= kTR - 1 || lj >= kTR - 1) continue;
-      shz[idx] = upd_h(shz[idx], sex[idx + 1], sex[idx], sey[idx + kTR], sey[idx]);
+      if (li >= kTR - 1 || gi >= nx - 1) continue;
+      const int l = li * kTR + lj;
+      float4 h = *reinterpret_cast<const float4*>(shz + l);
+      const float4 x = *reinterpret_cast<const float4*>(sex + l);
+      const float xr = lj + 4 < kTR ? sex[l + 4] : 0.f;
+      const float4 e = *reinterpret_cast<const float4*>(sey + l);
+      const float4 ed = *reinterpret_cast<const float4*>(sey + l + kTR);
+      const float hv[4] = {h.x, h.y, h.z, h.w}, xv[5] = {x.x, x.y, x.z, x.w, xr};
+      const float ev[4] = {e.x, e.y, e.z, e.w}, edv[4] = {ed.x, ed.y, ed.z, ed.w};
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        o[q] = gj + q < ny - 1 ? upd_h(hv[q], xv[q + 1], xv[q], edv[q], ev[q]) : hv[q];
+      h = make_float4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<float4*>(shz + l) = h;
     }
     __syncthreads();
   }
@@ -249,15 +281,16 @@ __global__ void __launch_bounds__(kTBThreads) step_tb(const float* __restrict__ 
   }
 }
 
-template <BenchId Bn, int V>
+template <BenchId Bn, int V, int kTB>
 void tb_sequence(Workspace& ws, cudaStream_t s) {
+  constexpr int kTT = kTR - 2 * kTB;
   const int nx = (int)ws.dims.d[0], ny = (int)ws.dims.d[1], tmax = (int)ws.dims.d[2];
   const size_t n = (size_t)nx * ny;
   float* scratch = ws.ensure_scratch(3 * n * sizeof(float));
   float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(step_tb<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem);
+    cudaFuncSetAttribute(step_tb<Bn, V, kTB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem);
     configured = true;
   }
   const dim3 grid(cdiv(ny, kTT), cdiv(nx, kTT));
@@ -265,21 +298,25 @@ void tb_sequence(Workspace& ws, cudaStream_t s) {
   for (int t = 0; t < tmax; t += kTB, ++launches) {
     float** src = buf[launches & 1];
     float** dst = buf[(launches + 1) & 1];
-    step_tb<Bn, V><<<grid, kTBThreads, kTBSmem, s>>>(ws.a.p[0], src[0], src[1], src[2], dst[0], dst[1], dst[2], nx, ny,
-                                                    t, std::min(kTB, tmax - t));
+    step_tb<Bn, V, kTB><<<grid, kTBThreads, kTBSmem, s>>>(ws.a.p[0], src[0], src[1], src[2], dst[0], dst[1], dst[2],
+                                                         nx, ny, t, std::min(kTB, tmax - t));
   }
   if (launches & 1)
     for (int f = 0; f < 3; ++f) cudaMemcpyAsync(buf[0][f], buf[1][f], n * sizeof(float), cudaMemcpyDeviceToDevice, s);
 }
 
-// PF_FDTD_TB=0: stage 2 replays the per-step fused sequence instead (A/B runs).
-inline bool fdtd_tb_disabled() {
-  static const bool d = [] {
+// Stage-2 time steps per launch: 4 by default (2048^2 x 500: 5.77 ms vs 6.16
+// ms for the per-step fused sequence); PF_FDTD_TB=0 selects the per-step
+// sequence, PF_FDTD_TB=8 a deeper blocking (6.47 ms; A/B runs).
+inline int fdtd_tb_depth() {
+  static const int d = [] {
     const char* e = std::getenv("PF_FDTD_TB");
-    return e && e[0] == '0';
+    const int v = e ? std::atoi(e) : 4;
+    return (v == 0 || v == 8) ? v : 4;  // depths keep region origins float4-aligned
   }();
   return d;
 }
+inline bool fdtd_tb_disabled() { return fdtd_tb_depth() == 0; }
 
 template <BenchId Bn, int V>
 void fused_sequence(Workspace& ws, cudaStream_t s) {
@@ -324,8 +361,10 @@ struct Run {
     } else {
       ws.ensure_scratch(3 * (size_t)nx * ny * sizeof(float));  // allocate before capture
       const bool tb = ny % 4 == 0 && !fdtd_tb_disabled();
-      cudaGraphExec_t g = tb ? cached_graph(ws, V, &tb_sequence<B_FDTD2D, V>)
-                             : cached_graph(ws, V + 1000, &fused_sequence<B_FDTD2D, V>);
+      const int d = fdtd_tb_depth();
+      cudaGraphExec_t g = !tb      ? cached_graph(ws, V + 1000, &fused_sequence<B_FDTD2D, V>)
+                          : d == 8 ? cached_graph(ws, V + 3000, &tb_sequence<B_FDTD2D, V, 8>)
+                                   : cached_graph(ws, V, &tb_sequence<B_FDTD2D, V, 4>);
       cudaGraphLaunch(g, s);
     }
   }
@@ -336,7 +375,7 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 int64_t elems(int a, const Dims& d) { return a == 0 ? d.d[2] : d.d[0] * d.d[1]; }
 int64_t launches(int v, const Dims& d) {
   const int st = kTab.v[v].stage;
-  if (st == 2 && d.d[1] % 4 == 0 && !fdtd_tb_disabled()) return (d.d[2] + kTB - 1) / kTB;
+  if (st == 2 && d.d[1] % 4 == 0 && !fdtd_tb_disabled()) return (d.d[2] + fdtd_tb_depth() - 1) / fdtd_tb_depth();
   return st == 0 ? 3 * d.d[2] : d.d[2];
 }
 // fused compulsory traffic per step: read ex, ey, hz, write ex, ey, hz

@@ -326,6 +326,7 @@ template <BenchId Bn, int V>
 __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict__ A, float* __restrict__ R,
                                                               float* __restrict__ Q, float* __restrict__ qbuf,
                                                               int* __restrict__ flags, int m, int n) {
+  int* colflags = flags + n;  // per-column flags (the next panel's owner), after the per-panel ones
   extern __shared__ __align__(16) float qpan[];  // [16][2048]: a panel's q vectors
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int b = blockIdx.x, c0 = b * kPanelW, w = min(kPanelW, n - c0);
@@ -353,7 +354,42 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   // ---- apply earlier panels: the whole panel's 16 q vectors (128 KB) are
   // copied into shared memory with cp.async behind one flag acquire, then
   // every warp applies them back to back with no further block barriers
+  // The panel right before this one is the critical path: its q vectors are
+  // consumed column by column (per-column flags) while its owner is still
+  // factoring, so only the last column's hand-over is exposed.
   for (int pb = 0; pb < b; ++pb) {
+    if (pb == b - 1) {
+      for (int kk = 0; kk < kPanelW; ++kk) {
+        const int k = pb * kPanelW + kk;
+        if (t == 0)
+          while (ld_acquire(colflags + k) == 0) {
+          }
+        __syncthreads();  // also: every warp is done with this slot's previous q
+        float* qb = qpan + (kk & 1) * kP2Rows;
+        const float4* qsrc = reinterpret_cast<const float4*>(qbuf + (size_t)k * kP2Rows);
+        reinterpret_cast<float4*>(qb)[t] = __ldcg(qsrc + t);
+        reinterpret_cast<float4*>(qb)[256 + t] = __ldcg(qsrc + 256 + t);
+        __syncthreads();
+        float q[64];
+#pragma unroll
+        for (int g = 0; g < 16; ++g) {
+          const float4 v = reinterpret_cast<const float4*>(qb)[32 * g + lane];
+          q[4 * g] = v.x;
+          q[4 * g + 1] = v.y;
+          q[4 * g + 2] = v.z;
+          q[4 * g + 3] = v.w;
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (2 * warp + c >= w) continue;
+          float r = dot64(q, a[c]);
+          if (lane == 0) R[(size_t)k * n + c0 + 2 * warp + c] = r;
+#pragma unroll
+          for (int i = 0; i < 64; ++i) a[c][i] = fmaf(-q[i], r, a[c][i]);
+        }
+      }
+      continue;
+    }
     if (t == 0)
       while (ld_acquire(flags + pb) == 0) {
       }
@@ -416,6 +452,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
           reinterpret_cast<float4*>(qg)[32 * g + lane] = v;
         }
         if (lane == 0) R[(size_t)k * n + k] = rkk;
+        __threadfence();  // q_k visible device-wide before its column flag
+        __syncwarp();
+        if (lane == 0) st_release(colflags + k, 1);
       };
       if (kk & 1)
         pivot(a[1], rdiag[1]);
@@ -472,10 +511,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
 template <BenchId Bn, int V>
 void launch_panel2(Workspace& ws, cudaStream_t s) {
   const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
-  float* scratch = ws.ensure_scratch((size_t)n * kP2Rows * sizeof(float) + (size_t)n * sizeof(int));
+  float* scratch = ws.ensure_scratch((size_t)n * kP2Rows * sizeof(float) + 2 * (size_t)n * sizeof(int));
   float* qbuf = scratch;
-  int* flags = reinterpret_cast<int*>(scratch + (size_t)n * kP2Rows);
-  cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), s);
+  int* flags = reinterpret_cast<int*>(scratch + (size_t)n * kP2Rows);  // [n] panel flags, [n] column flags
+  cudaMemsetAsync(flags, 0, 2 * (size_t)n * sizeof(int), s);
   float* A = ws.a.p[0];
   float* R = ws.a.p[1];
   float* Q = ws.a.p[2];
