@@ -322,15 +322,64 @@ __device__ __forceinline__ float dot64(const float (&x)[64], const float (&y)[64
   return warp_sum((s0 + s1) + (s2 + s3));
 }
 
+// Diagnostics (PF_GS_TRACE=1, timing studies only -- it overwrites zeros of
+// R's strict lower triangle): globaltimer in microseconds (mod 2^24) at
+// three points of CTA b, stored in R[n-1][3b .. 3b+2] when 3b+2 < n-1.
+__device__ __forceinline__ void gs_trace(float* R, int n, int b, int slot) {
+  if (3 * b + 2 >= n - 1) return;
+  uint64_t ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  R[(size_t)(n - 1) * n + 3 * b + slot] = (float)((ns / 1000) & 0xFFFFFF);
+}
+
+// One MGS step on a warp's two register columns: r_c = q . a_c (8
+// interleaved FMA chains, both butterflies interleaved), a_c -= r_c q, R row
+// entries stored by lane 0.  A column with use_c == false is left exactly
+// unchanged (r = 0) and its R entry is not written.
+__device__ __forceinline__ void update2(const float (&q)[64], float (&a)[2][64], bool use0, bool use1, float* rrow,
+                                        int lane) {
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 64; i += 4) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s[e] = fmaf(q[i + e], a[0][i + e], s[e]);
+      s[4 + e] = fmaf(q[i + e], a[1][i + e], s[4 + e]);
+    }
+  }
+  float r0 = (s[0] + s[1]) + (s[2] + s[3]), r1 = (s[4] + s[5]) + (s[6] + s[7]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+    r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+  }
+  r0 = use0 ? r0 : 0.f;
+  r1 = use1 ? r1 : 0.f;
+  if (lane == 0) {
+    if (use0) rrow[0] = r0;
+    if (use1) rrow[1] = r1;
+  }
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    a[0][i] = fmaf(-q[i], r0, a[0][i]);
+    a[1][i] = fmaf(-q[i], r1, a[1][i]);
+  }
+}
+
 template <BenchId Bn, int V>
 __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict__ A, float* __restrict__ R,
                                                               float* __restrict__ Q, float* __restrict__ qbuf,
-                                                              int* __restrict__ flags, int m, int n) {
+                                                              int* __restrict__ flags, int m, int n, int trace) {
   int* colflags = flags + n;  // per-column flags (the next panel's owner), after the per-panel ones
   extern __shared__ __align__(16) float qpan[];  // [16][2048]: a panel's q vectors
+  __shared__ __align__(8) uint64_t slot_bar[kPanelW];  // own panel: slot kk holds q_{c0+kk}
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int b = blockIdx.x, c0 = b * kPanelW, w = min(kPanelW, n - c0);
   float* st = qpan;  // staging for the panel load / store: 128 rows x 17
+  if (t < kPanelW) {  // ordered before use by the load loop's barriers
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&slot_bar[t]));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  }
   float a[2][64];
 
   // ---- load the panel (coalesced 16-float row segments through shared memory)
@@ -350,7 +399,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   }
   __syncthreads();
 
-  int step = 0;
+  if (trace && t == 0) gs_trace(R, n, b, 0);
   // ---- apply earlier panels: the whole panel's 16 q vectors (128 KB) are
   // copied into shared memory with cp.async behind one flag acquire, then
   // every warp applies them back to back with no further block barriers
@@ -359,17 +408,32 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   // factoring, so only the last column's hand-over is exposed.
   for (int pb = 0; pb < b; ++pb) {
     if (pb == b - 1) {
-      for (int kk = 0; kk < kPanelW; ++kk) {
-        const int k = pb * kPanelW + kk;
-        if (t == 0)
-          while (ld_acquire(colflags + k) == 0) {
+      // software pipeline, one block barrier per column: at iteration it the
+      // flag of column it is acquired and its copy issued (cp.async into its
+      // own slot), while column it-2 -- landed by now -- is applied
+      const uint32_t qs0 = static_cast<uint32_t>(__cvta_generic_to_shared(qpan));
+      for (int it = 0; it < kPanelW + 2; ++it) {
+        if (it < kPanelW && t == 0)
+          while (ld_acquire(colflags + pb * kPanelW + it) == 0) {
           }
-        __syncthreads();  // also: every warp is done with this slot's previous q
-        float* qb = qpan + (kk & 1) * kP2Rows;
-        const float4* qsrc = reinterpret_cast<const float4*>(qbuf + (size_t)k * kP2Rows);
-        reinterpret_cast<float4*>(qb)[t] = __ldcg(qsrc + t);
-        reinterpret_cast<float4*>(qb)[256 + t] = __ldcg(qsrc + 256 + t);
+        if (it < kPanelW)
+          asm volatile("cp.async.wait_group 1;" ::: "memory");  // own part of column it-2 landed
+        else if (it == kPanelW)
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
+        if (it < kPanelW) {
+          const float4* qsrc = reinterpret_cast<const float4*>(qbuf + (size_t)(pb * kPanelW + it) * kP2Rows);
+          const uint32_t d = qs0 + (uint32_t)(it * kP2Rows * 4);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * t), "l"(qsrc + t) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * (256 + t)), "l"(qsrc + 256 + t)
+                       : "memory");
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        if (it < 2) continue;
+        const int kk = it - 2, k = pb * kPanelW + kk;
+        const float* qb = qpan + kk * kP2Rows;
         float q[64];
 #pragma unroll
         for (int g = 0; g < 16; ++g) {
@@ -379,15 +443,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
           q[4 * g + 2] = v.z;
           q[4 * g + 3] = v.w;
         }
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          if (2 * warp + c >= w) continue;
-          float r = dot64(q, a[c]);
-          if (lane == 0) R[(size_t)k * n + c0 + 2 * warp + c] = r;
-#pragma unroll
-          for (int i = 0; i < 64; ++i) a[c][i] = fmaf(-q[i], r, a[c][i]);
-        }
+        update2(q, a, 2 * warp < w, 2 * warp + 1 < w, R + (size_t)k * n + c0 + 2 * warp, lane);
       }
+      __syncthreads();  // qpan is reused below
       continue;
     }
     if (t == 0)
@@ -415,31 +473,35 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
         q[4 * g + 2] = v.z;
         q[4 * g + 3] = v.w;
       }
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        if (2 * warp + c >= w) continue;
-        float r = dot64(q, a[c]);
-        if (lane == 0) R[(size_t)k * n + c0 + 2 * warp + c] = r;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) a[c][i] = fmaf(-q[i], r, a[c][i]);
-      }
+      update2(q, a, 2 * warp < w, 2 * warp + 1 < w, R + (size_t)k * n + c0 + 2 * warp, lane);
     }
   }
   __syncthreads();  // qpan is reused by the factorisation below
 
-  // ---- factor the own panel
+  if (trace && t == 0) gs_trace(R, n, b, 1);
+  // ---- factor the own panel.  Pivot warp kk/2 normalises column kk into
+  // shared slot kk (qpan is free again: 16 slots, never reused) and meets only
+  // the warps that still own a column > kk at a named barrier (bar.arrive if
+  // it is not one of them); finished warps drop out.  Warp 0, done after
+  // step 1, becomes the publisher: it copies ready slots to qbuf in batches,
+  // fences once per batch and raises their column flags, keeping the
+  // device-scope fence off the factorisation's critical path.
   float rdiag[2] = {1.f, 1.f};  // 1 / R[k][k] of the two own columns
-  for (int kk = 0; kk < w; ++kk, ++step) {
-    const int k = c0 + kk;
-    float* qb = qpan + (step & 1) * kP2Rows;
-    if (warp == kk / 2) {
+  const int last_warp = (w - 1) / 2;
+  for (int kk = 0; kk < w; ++kk) {
+    const int k = c0 + kk, pw = kk / 2;
+    const int my_last = min(2 * warp + 1, w - 1);  // highest own column
+    const bool consumer = 2 * warp < w && my_last > kk;
+    const bool producer = warp == pw;
+    if (!consumer && !producer) break;
+    float* qb = qpan + kk * kP2Rows;
+    if (producer) {
       // the pivot column's register slice is selected by a compile-time index
       // (a runtime a[kk & 1] would demote the whole panel to local memory)
       auto pivot = [&](float(&col)[64], float& rinv) {
         const float rkk = sqrtf(dot64(col, col));
         const float inv = 1.0f / rkk;
         rinv = inv;
-        float* qg = qbuf + (size_t)k * kP2Rows;
 #pragma unroll
         for (int g = 0; g < 16; ++g) {
           const int row = 128 * g + 4 * lane;
@@ -449,19 +511,25 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
           v.z = row + 2 < m ? col[4 * g + 2] * inv : 0.f;
           v.w = row + 3 < m ? col[4 * g + 3] * inv : 0.f;
           reinterpret_cast<float4*>(qb)[32 * g + lane] = v;
-          reinterpret_cast<float4*>(qg)[32 * g + lane] = v;
         }
         if (lane == 0) R[(size_t)k * n + k] = rkk;
-        __threadfence();  // q_k visible device-wide before its column flag
         __syncwarp();
-        if (lane == 0) st_release(colflags + k, 1);
+        if (lane == 0) {
+          const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&slot_bar[kk]));
+          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+        }
       };
       if (kk & 1)
         pivot(a[1], rdiag[1]);
       else
         pivot(a[0], rdiag[0]);
     }
-    __syncthreads();
+    const int nthreads = 32 * (last_warp - pw + 1);  // the pivot warp and every warp after it
+    if (consumer)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + (kk & 1)), "r"(nthreads) : "memory");
+    else
+      asm volatile("bar.arrive %0, %1;" ::"r"(1 + (kk & 1)), "r"(nthreads) : "memory");
+    if (!consumer) continue;  // (a pure producer has no later column: it leaves at the next check)
     float q[64];
 #pragma unroll
     for (int g = 0; g < 16; ++g) {
@@ -471,20 +539,53 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
       q[4 * g + 2] = v.z;
       q[4 * g + 3] = v.w;
     }
+    update2(q, a, 2 * warp < w && 2 * warp > kk, 2 * warp + 1 < w && 2 * warp + 1 > kk,
+            R + (size_t)k * n + c0 + 2 * warp, lane);
+  }
+  if (warp == 0) {  // publisher
+    auto ready = [&](int j, bool block) {
+      const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&slot_bar[j]));
+      uint32_t ok = 0;
+      do {
+        if (block)
+          asm volatile(
+              "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], 0;\n\t"
+              "selp.b32 %0, 1, 0, P;\n\t}"
+              : "=r"(ok)
+              : "r"(bar)
+              : "memory");
+        else
+          asm volatile(
+              "{\n\t.reg .pred P;\n\tmbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P, [%1], 0;\n\t"
+              "selp.b32 %0, 1, 0, P;\n\t}"
+              : "=r"(ok)
+              : "r"(bar)
+              : "memory");
+      } while (block && !ok);
+      return ok != 0;
+    };
+    for (int next = 0; next < w;) {
+      ready(next, true);
+      int last = next;
+      while (last + 1 < w && last + 1 < next + 4 && ready(last + 1, false)) ++last;
+      for (int j = next; j <= last; ++j) {
+        const float4* src = reinterpret_cast<const float4*>(qpan + j * kP2Rows);
+        float4* dst = reinterpret_cast<float4*>(qbuf + (size_t)(c0 + j) * kP2Rows);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int jj = 2 * warp + c;
-      if (jj >= w || jj <= kk) continue;
-      float r = dot64(q, a[c]);
-      if (lane == 0) R[(size_t)k * n + c0 + jj] = r;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) a[c][i] = fmaf(-q[i], r, a[c][i]);
+        for (int g = 0; g < 16; ++g) dst[32 * g + lane] = src[32 * g + lane];
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0)
+        for (int j = next; j <= last; ++j) st_release(colflags + c0 + j, 1);
+      next = last + 1;
     }
   }
   // ---- publish the panel's q vectors
   __threadfence();
   __syncthreads();
   if (t == 0) st_release(flags + b, 1);
+  if (trace && t == 0) gs_trace(R, n, b, 2);
 
   // ---- write back A (final columns) and Q = A / R[k][k] (coalesced through shared memory)
 #pragma unroll 1
@@ -518,7 +619,11 @@ void launch_panel2(Workspace& ws, cudaStream_t s) {
   float* A = ws.a.p[0];
   float* R = ws.a.p[1];
   float* Q = ws.a.p[2];
-  void* args[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n};
+  static const int trace = [] {
+    const char* e = std::getenv("PF_GS_TRACE");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  void* args[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n, (void*)&trace};
   const int grid = (n + kPanelW - 1) / kPanelW;
   constexpr size_t smem = (size_t)kPanelW * kP2Rows * sizeof(float);
   static bool configured = false;
