@@ -178,6 +178,14 @@ void register_bench(int id, const BenchDesc* desc) {
   if (id >= 0 && id < B_COUNT) registry()[id] = desc;
 }
 
+int* Workspace::ensure_tile_flags() {
+  if (tile_flags) return tile_flags;
+  if (cudaMalloc(&tile_flags, kTileFlags * sizeof(int)) != cudaSuccess) return tile_flags = nullptr;
+  cudaMemset(tile_flags, 0, kTileFlags * sizeof(int));  // first use is outside timed regions (warm-up)
+  tile_epoch = 0;
+  return tile_flags;
+}
+
 float* Workspace::ensure_scratch(size_t bytes) {
   if (scratch_bytes >= bytes) return scratch;
   if (scratch) cudaFree(scratch);
@@ -381,6 +389,7 @@ int pf_ws_destroy(pf_ws* ws) {
     if (ws->pristine[a]) cudaFree(ws->pristine[a]);
   }
   if (ws->scratch) cudaFree(ws->scratch);
+  if (ws->tile_flags) cudaFree(ws->tile_flags);
   if (ws->graphs) {
     auto* gc = static_cast<GraphCache*>(ws->graphs);
     for (auto& kv : gc->exec) cudaGraphExecDestroy(kv.second);

@@ -248,7 +248,9 @@ inline void run(Workspace& ws, cudaStream_t s) {
       float* G = xt + (size_t)m * np;
       reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, 32), cdiv(n, 32)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt, m,
                                                                                            n, np);
-      const TcGemmArgs g{m, m, n, 1.f, 0.f, xt, np, false, xt, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
+      TcGemmArgs g{m, m, n, 1.f, 0.f, xt, np, false, xt, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
+      g.tile_flags = ws.ensure_tile_flags();
+      g.epoch = ++ws.tile_epoch;
       if (!launch_tc_tma<Bn, V>(g, s)) {
         launch_failed("CORR/COVAR stage 2: TMA operand maps rejected");
         return;
@@ -269,7 +271,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
 inline int64_t launches(bool corr, int stage, int64_t m, int64_t n) {
   if (stage == 0) return corr ? 4 : 3;
   const int64_t stats = corr ? 4 : 2;
-  if (stage == 2) return stats + 1 + tc_tma_launches(m, m, n, false, true) + 1;
+  if (stage == 2) return stats + 1 + tc_tma_launches(m, m, n, false, true, true) + 1;
   return stats + 1 + 1 + 1 + (corr ? 1 : 0);
 }
 

@@ -103,7 +103,14 @@ struct Workspace {
   float* scratch;        // lazily grown temporary buffer for variants that need one
   size_t scratch_bytes;
   float* ensure_scratch(size_t bytes);  // defined in abi.cu; only called outside timed regions' first use
+  // split-K tile hand-over flags (tcgen05 contractions): kTileFlags ints,
+  // zeroed once; each launch uses a fresh epoch value (runs on a workspace
+  // are serialised on its stream, so epochs never interleave)
+  int* tile_flags;
+  int tile_epoch;
+  int* ensure_tile_flags();  // defined in abi.cu
 };
+constexpr int kTileFlags = 4096;
 
 // Graph-staged variants: capture `body` once per (workspace, key) and return
 // the executable graph (abi.cu).  Launch with cudaGraphLaunch(exec, stream).

@@ -51,6 +51,10 @@ struct TcGemmArgs {
   const float* Blo = nullptr;
   const float* A2lo = nullptr;
   const float* B2lo = nullptr;
+  // split-K hand-over flags (Workspace::ensure_tile_flags) and this launch's
+  // epoch; nullptr: split-K products use a beta pre-pass instead
+  int* tile_flags = nullptr;
+  int epoch = 0;
 };
 
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;

@@ -47,6 +47,8 @@ struct TmaParams {
   int presplit;
   CUtensorMap tc, td;            // epilogue: Cin / D as 32x32 SWIZZLE_128B boxes (valid iff tma_epi)
   int tma_epi;
+  int* tile_flags;               // ordered split-K: split 0 stores, the others add after its flag
+  int epoch;
   int creduce;                   // split-K partials reduced across the z-cluster through DSMEM (tc_tma_kernel)
   int kblocks, kb_per_split, kb1;
   int a_mn, b_mn;                // operand is MN-major (contiguous along M / N)
@@ -136,7 +138,8 @@ __device__ __forceinline__ void reduce_add_2d(const CUtensorMap* map, uint32_t s
 // (or a TMA add-reduction onto the beta-prescaled D for split-K).  buf:
 // 1024-byte aligned, ncols / 32 * 4 KB; bar: this warp's mbarrier (phase 0).
 __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr, int ncols, int row0, int col0,
-                                             bool split, uint8_t* buf, uint32_t bar, int lane) {
+                                             bool split, uint8_t* buf, uint32_t bar, int lane,
+                                             bool writes_done = false) {
   if (row0 >= p.M) return;  // warp-uniform
   const int nch = min(ncols / 32, (p.N - col0 + 31) / 32);
   const bool use_c = !split && p.beta != 0.f;
@@ -173,8 +176,39 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr,
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  if (lane == 0) {
+    if (writes_done)  // the stores themselves complete (split-K hand-over), not just their smem reads
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    else
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
   __syncwarp();
+}
+
+// Ordered split-K hand-over.  Split 0 of an output tile writes
+// alpha * acc + beta * Cin with plain TMA stores and then raises the tile's
+// flag to this launch's epoch; every other split waits for that flag before
+// its TMA add-reductions.  No beta pre-pass kernel, no extra launch.
+__device__ __forceinline__ void split_wait(const TmaParams& p, int lane) {
+  const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+  if (lane == 0) {
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.tile_flags + tile) : "memory");
+    } while (v != p.epoch);
+  }
+  __syncwarp();
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // the add-reductions (async proxy) come after
+}
+
+__device__ __forceinline__ void split_publish(const TmaParams& p, int warp, int lane) {
+  asm volatile("bar.sync 3, 128;" ::: "memory");  // the four epilogue warps' stores are complete
+  if (warp == 2 && lane == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.tile_flags + tile), "r"(p.epoch) : "memory");
+  }
 }
 
 // The A and B tiles of one k block (raw, or the pre-split lo images) into
@@ -388,9 +422,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
     const int quad = warp & 3;
     if (p.creduce)
       tma::stage_partial(tmem + ((uint32_t)(quad * 32) << 16), smem, quad * 32 + lane);
-    else if (p.tma_epi && !(p.diag & (8 | 16 | 32)))
-      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, split,
-                        smem + (size_t)quad * 32768, tc::smem_u32(&epi_bar[quad]), lane);
+    else if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
+      const bool ordered = split && p.tile_flags != nullptr;
+      if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
+      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
+                        split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
+                        tc::smem_u32(&epi_bar[quad]), lane, ordered);
+      if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
+    }
     else if (p.diag & 16)
       tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                              p.Cin, p.ldc, p.D, p.ldd, split, lane);
@@ -598,9 +637,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
     tc2::wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
     const int quad = warp & 3;
-    if (p.tma_epi && !(p.diag & (8 | 16 | 32)))
-      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, split,
-                        smem + (size_t)quad * 32768, tc::smem_u32(&epi_bar[quad]), lane);
+    if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
+      const bool ordered = split && p.tile_flags != nullptr;
+      if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
+      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
+                        split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
+                        tc::smem_u32(&epi_bar[quad]), lane, ordered);
+      if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
+    }
     else if (p.diag & 16)
       tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                              p.Cin, p.ldc, p.D, p.ldd, split, lane);
@@ -782,7 +826,15 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
   const bool pair = !p.creduce && tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
   const int zs = p.creduce ? cz : tc_tma_splits(a.M, a.N, kblocks, pair, up);
   const int per = (kblocks + zs - 1) / zs;
-  if (zs > 1 && !p.creduce) {
+  const int64_t grid_tiles = pair ? 2 * cdiv(a.N, 256) * (int64_t)cdiv(a.M, 256) : (int64_t)cdiv(a.N, 128) * cdiv(a.M, 128);
+  // ordered hand-over only where the alternative pre-pass is a memset (beta
+  // == 0): with beta != 0 split 0's Cin load + store serialise the splits
+  // (GEMM 512^3: 17.4 us vs 15.3 us with the beta pre-pass)
+  const bool ordered =
+      zs > 1 && !p.creduce && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlags && a.beta == 0.f;
+  p.tile_flags = ordered ? a.tile_flags : nullptr;
+  p.epoch = a.epoch;
+  if (zs > 1 && !p.creduce && !ordered) {
     if (a.beta == 0.f)
       cudaMemset2DAsync(a.D, (size_t)a.ldd * sizeof(float), 0, (size_t)a.N * sizeof(float), a.M, s);
     else
@@ -829,11 +881,13 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
 }
 
 // launches of one TMA-path product: [prescale] + gemm
-inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false, bool upper = false) {
+inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false, bool upper = false,
+                               bool beta_zero = false) {
   const int kblocks = (int)((dual ? 2 : 1) * ((k + 31) / 32));
   if (tc_cluster_splits(m, n, kblocks) > 1) return 1;
   const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, upper) <= 2;
-  return tc_tma_splits(m, n, kblocks, pair, upper) > 1 ? 2 : 1;
+  const bool split = tc_tma_splits(m, n, kblocks, pair, upper) > 1;
+  return split && !beta_zero ? 2 : 1;  // beta pre-pass, or the in-kernel ordered hand-over
 }
 
 }  // namespace pf
@@ -877,7 +931,9 @@ inline bool tc_presplit_wanted(int64_t m, int64_t n, int64_t k, bool dual, bool 
     return v ? std::atoi(v) : -1;
   }();
   if (mode >= 0) return mode == 1;
-  return tc_tma_launches(m, n, k, dual, upper) == 1;
+  const int kblocks = (int)((dual ? 2 : 1) * ((k + 31) / 32));
+  const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, upper) <= 2;
+  return tc_tma_splits(m, n, kblocks, pair, upper) == 1;
 }
 
 // launches of one contraction: [lo passes, one per distinct operand array] +
@@ -888,7 +944,10 @@ inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual,
 }
 
 template <BenchId Bn, int V>
-inline void launch_contraction(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
+inline void launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t s) {
+  TcGemmArgs a = a0;
+  a.tile_flags = ws.ensure_tile_flags();
+  a.epoch = ++ws.tile_epoch;
   if (tc_presplit_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0) && tma_ok(a.lda, a.ldb)) {
     // distinct operand arrays and their storage extents (floats)
     const float* ops[4] = {a.A, a.B, a.A2, a.B2};
