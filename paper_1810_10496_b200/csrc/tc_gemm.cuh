@@ -424,6 +424,10 @@ inline bool tc_gemm_supported(int64_t m, int64_t n, int64_t k) { return m > 0 &&
 template <BenchId Bn, int V>
 __global__ void __launch_bounds__(256) tc_prescale(float* D, int ldd, const float* Cin, int ldc, int M, int N,
                                                    float beta) {
+  // the split-K GEMM launched after this kernel (programmatic dependent
+  // launch) may start its mainloop now; it waits for this grid before its
+  // first add-reduction onto D
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const int m = blockIdx.y;
   if (n >= N) return;

@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
     else if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
+      if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
       tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered);
@@ -640,6 +641,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
     if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
+      if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
       tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered);
@@ -873,10 +875,25 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, tc_tma_kernel<Bn, V>, p) != cudaSuccess)
       launch_failed("tcgen05 split-K cluster launch rejected");
-  } else if (pair)
-    tc_tma2_kernel<Bn, V><<<dim3(2 * cdiv(a.N, 256), cdiv(a.M, 256), zs), kTmaThreads, kTmaSmem, s>>>(p);
-  else
-    tc_tma_kernel<Bn, V><<<dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs), kTmaThreads, kTmaSmem, s>>>(p);
+  } else {
+    // after a beta pre-pass the GEMM is a programmatic dependent launch: its
+    // prologue and mainloop overlap the pre-pass (griddepcontrol.wait gates
+    // only the epilogue's add-reductions)
+    const bool pdl = zs > 1 && !ordered;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = pair ? dim3(2 * cdiv(a.N, 256), cdiv(a.M, 256), zs) : dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs);
+    cfg.blockDim = dim3(kTmaThreads);
+    cfg.dynamicSmemBytes = kTmaSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const cudaError_t e = pair ? cudaLaunchKernelEx(&cfg, tc_tma2_kernel<Bn, V>, p)
+                               : cudaLaunchKernelEx(&cfg, tc_tma_kernel<Bn, V>, p);
+    if (e != cudaSuccess) launch_failed("tcgen05 contraction launch rejected");
+  }
   return true;
 }
 
