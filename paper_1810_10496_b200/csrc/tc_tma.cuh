@@ -924,8 +924,19 @@ inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual 
 // lo = x - trunc_tf32(x) over n floats (operand storage, pitch included)
 template <BenchId Bn, int V>
 __global__ void __launch_bounds__(256) tc_split_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
-  const int64_t n4 = n / 4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {  // four 16-byte loads in flight per thread
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(x) + i + u * stride);  // the GEMM re-reads x from L2
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      reinterpret_cast<float4*>(lo)[i + u * stride] =
+          make_float4(v[u].x - tma::trunc_tf32(v[u].x), v[u].y - tma::trunc_tf32(v[u].y),
+                      v[u].z - tma::trunc_tf32(v[u].z), v[u].w - tma::trunc_tf32(v[u].w));
+  }
+  for (; i < n4; i += stride) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
     reinterpret_cast<float4*>(lo)[i] = make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
                                                    v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w));

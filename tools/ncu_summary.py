@@ -23,6 +23,9 @@ KEYS = [
     ("launch__registers_per_thread", "regs/thread"),
     ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe active %"),
     ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "TC smem operand wavefronts %"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tcgen05 tensor datapath active % (of active cycles)"),
+    ("smsp__inst_executed.sum", "warp instructions executed"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
 ]
 
