@@ -332,6 +332,16 @@ __device__ __forceinline__ void gs_trace(float* R, int n, int b, int slot) {
   R[(size_t)(n - 1) * n + 3 * b + slot] = (float)((ns / 1000) & 0xFFFFFF);
 }
 
+// Diagnostics: step-level timeline of CTA 5's own-panel factorisation in R's
+// row n-2 (strict lower triangle): [3kk] pivot done, [3kk+1] last warp past
+// the barrier, [3kk+2] last warp's update done (microseconds, mod 2^24).
+__device__ __forceinline__ void gs_trace_step(float* R, int n, int kk, int slot) {
+  if (3 * kk + slot >= n - 2) return;
+  uint64_t ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  R[(size_t)(n - 2) * n + 3 * kk + slot] = (float)((ns / 10) & 0xFFFFFF) * 0.01f;
+}
+
 // One MGS step on a warp's two register columns: r_c = q . a_c (8
 // interleaved FMA chains, both butterflies interleaved), a_c -= r_c q, R row
 // entries stored by lane 0.  A column with use_c == false is left exactly
@@ -523,6 +533,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
         pivot(a[1], rdiag[1]);
       else
         pivot(a[0], rdiag[0]);
+      if (trace && b == 5 && lane == 0) gs_trace_step(R, n, kk, 0);
     }
     const int nthreads = 32 * (last_warp - pw + 1);  // the pivot warp and every warp after it
     if (consumer)
@@ -530,6 +541,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
     else
       asm volatile("bar.arrive %0, %1;" ::"r"(1 + (kk & 1)), "r"(nthreads) : "memory");
     if (!consumer) continue;  // (a pure producer has no later column: it leaves at the next check)
+    if (trace && b == 5 && warp == last_warp && lane == 0) gs_trace_step(R, n, kk, 1);
     float q[64];
 #pragma unroll
     for (int g = 0; g < 16; ++g) {
@@ -541,6 +553,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
     }
     update2(q, a, 2 * warp < w && 2 * warp > kk, 2 * warp + 1 < w && 2 * warp + 1 > kk,
             R + (size_t)k * n + c0 + 2 * warp, lane);
+    if (trace && b == 5 && warp == last_warp && lane == 0) gs_trace_step(R, n, kk, 2);
   }
   if (warp == 0) {  // publisher
     auto ready = [&](int j, bool block) {
