@@ -349,119 +349,6 @@ __global__ void __launch_bounds__(TX * TY) conv3d_s2d(const float* __restrict__ 
   }
 }
 
-// Stage 2, cp.async form: the input planes of a (4 rows x 256 k) output tile
-// stream through a kCS-deep shared-memory ring filled with cp.async (16-byte
-// LDGSTS, zero-filled outside the volume), so loads in flight cost no
-// registers -- (kCS - 1) planes x 6 rows x 1 KB per block.  One block barrier
-// per plane: the slot refilled at iteration q is the one consumed at q - 1.
-// Each thread computes 2 rows x 4 k with the folded 11-FMA taps.
-constexpr int kCS = 4;                 // ring depth (planes)
-constexpr int kCW = 256;               // output k per block
-constexpr int kCRow = kCW + 8;         // smem row: k0-4 .. k0+259
-constexpr int kCRows = 6;              // 4 output rows + halo
-constexpr int kCPlane = kCRows * kCRow;
-constexpr int kCCH = 16;               // output planes per block
-constexpr size_t kCSmem = (size_t)kCS * kCPlane * sizeof(float);
-
-__device__ __forceinline__ void c3_issue_plane(float* ring, const float* __restrict__ A, int q, int ni, int nj, int nk,
-                                               int j0, int k0) {
-  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(ring + (q % kCS) * kCPlane));
-  constexpr int kV = kCRow / 4;  // float4 per smem row (66)
-  for (int idx = threadIdx.x + blockDim.x * threadIdx.y; idx < kCRows * kV; idx += blockDim.x * blockDim.y) {
-    const int rr = idx / kV, v = idx % kV;
-    const int row = j0 - 1 + rr, k = k0 - 4 + 4 * v;
-    const bool in = q < ni && row < nj && k >= 0 && k < nk;
-    const float* src = in ? A + ((size_t)q * nj + row) * nk + k : A;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(base + 16u * (rr * kV + v)), "l"(src),
-                 "r"(in ? 16 : 0)
-                 : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <BenchId Bn, int V>
-__global__ void __launch_bounds__(128) conv3d_s2c(const float* __restrict__ A, float* __restrict__ B, int ni, int nj,
-                                                  int nk) {
-  extern __shared__ __align__(16) float c3_ring[];
-  const int k0 = blockIdx.x * kCW, j0 = 1 + blockIdx.y * 4;  // output rows j0 .. j0+3
-  const int i0 = 1 + blockIdx.z * kCCH, i1 = min(ni - 1, i0 + kCCH);
-  const int tx = threadIdx.x, ty = threadIdx.y;            // 64 x 2
-  const int kq = k0 + 4 * tx, jr = j0 + 2 * ty;              // this thread: rows jr, jr+1; k kq .. kq+3
-  const int nq = i1 - i0 + 2;                                // input planes i0-1 .. i1
-  constexpr float cM = c11 + c21 + c31, cP = c13 + c23 + c33;
-#pragma unroll
-  for (int d = 0; d < kCS - 1; ++d) {
-    if (d < nq)
-      c3_issue_plane(c3_ring, A, i0 - 1 + d, ni, nj, nk, j0, k0);
-    else
-      asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  float mz[2][4], mn[2][4];
-#pragma unroll
-  for (int r = 0; r < 2; ++r)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) mz[r][e] = mn[r][e] = 0.f;
-  const bool full = kq >= 1 && kq + 4 <= nk - 1;
-  for (int q = 0; q < nq; ++q) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(kCS - 2) : "memory");  // plane q landed (own part)
-    __syncthreads();                                                      // ... everyone's; slot q-1 free
-    if (q + kCS - 1 < nq)
-      c3_issue_plane(c3_ring, A, i0 - 1 + q + kCS - 1, ni, nj, nk, j0, k0);
-    else
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    const float* pl = c3_ring + (q % kCS) * kCPlane;
-    float v[4][6];  // rows jr-1 .. jr+2, columns kq-1 .. kq+4
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const float* row = pl + (2 * ty + rr) * kCRow + 4 + 4 * tx;
-      const float4 c = *reinterpret_cast<const float4*>(row);
-      v[rr][0] = row[-1];
-      v[rr][1] = c.x;
-      v[rr][2] = c.y;
-      v[rr][3] = c.z;
-      v[rr][4] = c.w;
-      v[rr][5] = row[4];
-    }
-    if (kq >= nk) continue;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      float out[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float xmm = v[r][e], xmz = v[r][e + 1], xmp = v[r][e + 2];
-        const float xzz = v[r + 1][e + 1], xzp = v[r + 1][e + 2];
-        const float xpz = v[r + 2][e + 1], xpp = v[r + 2][e + 2];
-        out[e] = fmaf(c33, xpp, fmaf(c23, xzp, fmaf(c13, xmp, fmaf(cP, xmm, mz[r][e]))));
-        mz[r][e] = fmaf(c32, xpz, fmaf(c22, xzz, fmaf(c12, xmz, mn[r][e])));
-        mn[r][e] = fmaf(c31, xpp, fmaf(c21, xzp, fmaf(c11, xmp, cM * xmm)));
-      }
-      const int i = i0 + q - 2, j = jr + r;
-      if (q >= 2 && j <= nj - 2) {
-        float* o = B + ((size_t)i * nj + j) * nk + kq;
-        if (full) {
-          __stcs(reinterpret_cast<float4*>(o), make_float4(out[0], out[1], out[2], out[3]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (kq + e >= 1 && kq + e <= nk - 2) o[e] = out[e];
-        }
-      }
-    }
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
-template <int V>
-void launch_s2c(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(conv3d_s2c<B_3DCONV, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCSmem);
-    configured = true;
-  }
-  conv3d_s2c<B_3DCONV, V><<<dim3(cdiv(nk, kCW), cdiv(nj - 2, 4), cdiv(ni - 2, kCCH)), dim3(64, 2), kCSmem, s>>>(
-      A, B, ni, nj, nk);
-}
-
 template <int V, int R, int PD, int CH, int TX, int TY, int KV>
 void launch_s2d(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s) {
   if constexpr (KV > 1) {
@@ -474,8 +361,11 @@ void launch_s2d(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s
                                                    dim3(TX, TY), 0, s>>>(A, B, ni, nj, nk);
 }
 
-// PF_C3 (A/B runs): "t" = TMA plane-streaming kernel, "0".."3" = direct-form
-// configurations; default = direct form 0.
+// PF_C3=t (A/B runs) selects the TMA plane-streaming kernel (38.9 us at 256^3,
+// issue-bound); default: the direct form (2 rows x float4 per thread, 8-plane
+// chunks, 2 planes of register prefetch: 28.6 us).  Shapes measured and
+// dropped: 4- and 32-plane chunks, 1 or 4 rows, 3-4 planes of prefetch, two
+// float4 per thread, and a cp.async shared-memory ring (37 us).
 inline int c3_mode() {
   static const int m = [] {
     const char* e = std::getenv("PF_C3");
@@ -530,14 +420,6 @@ struct Run {
     } else {
       switch (c3_mode()) {
         case -1: launch_s2<V>(A, B, ni, nj, nk, s); break;
-        case 9: launch_s2c<V>(A, B, ni, nj, nk, s); break;
-        case 1: launch_s2d<V, 2, 2, 4, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        case 2: launch_s2d<V, 2, 2, 32, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        case 3: launch_s2d<V, 2, 1, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        case 4: launch_s2d<V, 1, 2, 8, 64, 4, 1>(A, B, ni, nj, nk, s); break;
-        case 5: launch_s2d<V, 2, 2, 8, 32, 4, 1>(A, B, ni, nj, nk, s); break;
-        case 6: launch_s2d<V, 2, 3, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
-        case 7: launch_s2d<V, 2, 2, 16, 64, 2, 1>(A, B, ni, nj, nk, s); break;
         default: launch_s2d<V, 2, 2, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
       }
     }

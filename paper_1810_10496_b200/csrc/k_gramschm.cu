@@ -334,12 +334,13 @@ __device__ __forceinline__ void gs_trace(float* R, int n, int b, int slot) {
 
 // Diagnostics: step-level timeline of CTA 5's own-panel factorisation in R's
 // row n-2 (strict lower triangle): [3kk] pivot done, [3kk+1] last warp past
-// the barrier, [3kk+2] last warp's update done (microseconds, mod 2^24).
+// the barrier, [3kk+2] last warp's update done, [3kk+3] pivot warp starts its
+// pivot (microseconds, mod 2^24; layout 4 per step).
 __device__ __forceinline__ void gs_trace_step(float* R, int n, int kk, int slot) {
-  if (3 * kk + slot >= n - 2) return;
+  if (4 * kk + slot >= n - 2) return;
   uint64_t ns;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-  R[(size_t)(n - 2) * n + 3 * kk + slot] = (float)((ns / 10) & 0xFFFFFF) * 0.01f;
+  R[(size_t)(n - 2) * n + 4 * kk + slot] = (float)((ns / 10) & 0xFFFFFF) * 0.01f;
 }
 
 // One MGS step on a warp's two register columns: r_c = q . a_c (8
@@ -376,17 +377,19 @@ __device__ __forceinline__ void update2(const float (&q)[64], float (&a)[2][64],
   }
 }
 
-template <BenchId Bn, int V>
-__global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict__ A, float* __restrict__ R,
+template <BenchId Bn, int V, int W>
+__global__ void __launch_bounds__(16 * W, 1) gs_panel2(float* __restrict__ A, float* __restrict__ R,
                                                               float* __restrict__ Q, float* __restrict__ qbuf,
                                                               int* __restrict__ flags, int m, int n, int trace) {
+  constexpr int NT = 16 * W;  // W/2 warps, two register columns each
   int* colflags = flags + n;  // per-column flags (the next panel's owner), after the per-panel ones
   extern __shared__ __align__(16) float qpan[];  // [16][2048]: a panel's q vectors
-  __shared__ __align__(8) uint64_t slot_bar[kPanelW];  // own panel: slot kk holds q_{c0+kk}
+  __shared__ __align__(8) uint64_t slot_bar[W];  // own panel: slot kk holds q_{c0+kk}
+  __shared__ float rbuf[W * W];                  // own panel's R block, written out after the factorisation
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int b = blockIdx.x, c0 = b * kPanelW, w = min(kPanelW, n - c0);
-  float* st = qpan;  // staging for the panel load / store: 128 rows x 17
-  if (t < kPanelW) {  // ordered before use by the load loop's barriers
+  const int b = blockIdx.x, c0 = b * W, w = min(W, n - c0);
+  float* st = qpan;  // staging for the panel load / store: 128 rows x (W + 1)
+  if (t < W) {  // ordered before use by the load loop's barriers
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&slot_bar[t]));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
   }
@@ -398,14 +401,14 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int idx = t + 256 * e, row = 128 * P + idx / 16, col = idx % 16;
-      st[(idx / 16) * 17 + col] = (row < m && col < w) ? A[(size_t)row * n + c0 + col] : 0.f;
+      const int idx = t + NT * e, row = 128 * P + idx / W, col = idx % W;
+      st[(idx / W) * (W + 1) + col] = (row < m && col < w) ? A[(size_t)row * n + c0 + col] : 0.f;
     }
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 4; ++e)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) a[c][4 * P + e] = st[(4 * lane + e) * 17 + 2 * warp + c];
+      for (int c = 0; c < 2; ++c) a[c][4 * P + e] = st[(4 * lane + e) * (W + 1) + 2 * warp + c];
   }
   __syncthreads();
 
@@ -422,27 +425,29 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
       // flag of column it is acquired and its copy issued (cp.async into its
       // own slot), while column it-2 -- landed by now -- is applied
       const uint32_t qs0 = static_cast<uint32_t>(__cvta_generic_to_shared(qpan));
-      for (int it = 0; it < kPanelW + 2; ++it) {
-        if (it < kPanelW && t == 0)
-          while (ld_acquire(colflags + pb * kPanelW + it) == 0) {
+      for (int it = 0; it < W + 2; ++it) {
+        if (it < W && t == 0)
+          while (ld_acquire(colflags + pb * W + it) == 0) {
           }
-        if (it < kPanelW)
+        if (it < W)
           asm volatile("cp.async.wait_group 1;" ::: "memory");  // own part of column it-2 landed
-        else if (it == kPanelW)
+        else if (it == W)
           asm volatile("cp.async.wait_group 1;" ::: "memory");
         else
           asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
-        if (it < kPanelW) {
-          const float4* qsrc = reinterpret_cast<const float4*>(qbuf + (size_t)(pb * kPanelW + it) * kP2Rows);
+        if (it < W) {
+          const float4* qsrc = reinterpret_cast<const float4*>(qbuf + (size_t)(pb * W + it) * kP2Rows);
           const uint32_t d = qs0 + (uint32_t)(it * kP2Rows * 4);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * t), "l"(qsrc + t) : "memory");
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * (256 + t)), "l"(qsrc + 256 + t)
-                       : "memory");
+#pragma unroll
+          for (int u = 0; u < kP2Rows / 4 / NT; ++u)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * (NT * u + t)),
+                         "l"(qsrc + NT * u + t)
+                         : "memory");
           asm volatile("cp.async.commit_group;" ::: "memory");
         }
         if (it < 2) continue;
-        const int kk = it - 2, k = pb * kPanelW + kk;
+        const int kk = it - 2, k = pb * W + kk;
         const float* qb = qpan + kk * kP2Rows;
         float q[64];
 #pragma unroll
@@ -462,17 +467,17 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
       while (ld_acquire(flags + pb) == 0) {
       }
     __syncthreads();  // also: every warp is done with the previous panel's q
-    const float4* src = reinterpret_cast<const float4*>(qbuf + (size_t)pb * kPanelW * kP2Rows);
+    const float4* src = reinterpret_cast<const float4*>(qbuf + (size_t)pb * W * kP2Rows);
     const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(qpan));
 #pragma unroll 8
-    for (int e = 0; e < kPanelW * kP2Rows / 4 / kPanelThreads; ++e) {
-      const int idx = t + kPanelThreads * e;
+    for (int e = 0; e < W * kP2Rows / 4 / NT; ++e) {
+      const int idx = t + NT * e;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * idx), "l"(src + idx) : "memory");
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    for (int kk = 0; kk < kPanelW; ++kk) {
-      const int k = pb * kPanelW + kk;
+    for (int kk = 0; kk < W; ++kk) {
+      const int k = pb * W + kk;
       const float* qb = qpan + kk * kP2Rows;
       float q[64];
 #pragma unroll
@@ -499,31 +504,30 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   float rdiag[2] = {1.f, 1.f};  // 1 / R[k][k] of the two own columns
   const int last_warp = (w - 1) / 2;
   for (int kk = 0; kk < w; ++kk) {
-    const int k = c0 + kk, pw = kk / 2;
+    const int pw = kk / 2;
     const int my_last = min(2 * warp + 1, w - 1);  // highest own column
     const bool consumer = 2 * warp < w && my_last > kk;
     const bool producer = warp == pw;
     if (!consumer && !producer) break;
     float* qb = qpan + kk * kP2Rows;
     if (producer) {
+      if (trace && b == 5 && lane == 0) gs_trace_step(R, n, kk, 3);
       // the pivot column's register slice is selected by a compile-time index
       // (a runtime a[kk & 1] would demote the whole panel to local memory)
+      // One warp runs this while the others wait, so it is kept short: rows
+      // >= m are exactly zero in every register column (loaded as zero, and
+      // q is zero there), so no row masks; 1/R[k][k] from one MUFU.RSQ.
       auto pivot = [&](float(&col)[64], float& rinv) {
-        const float rkk = sqrtf(dot64(col, col));
-        const float inv = 1.0f / rkk;
+        const float nrm = dot64(col, col);
+        const float inv = rsqrtf(nrm);
+        const float rkk = nrm * inv;
         rinv = inv;
 #pragma unroll
-        for (int g = 0; g < 16; ++g) {
-          const int row = 128 * g + 4 * lane;
-          float4 v;
-          v.x = row < m ? col[4 * g] * inv : 0.f;
-          v.y = row + 1 < m ? col[4 * g + 1] * inv : 0.f;
-          v.z = row + 2 < m ? col[4 * g + 2] * inv : 0.f;
-          v.w = row + 3 < m ? col[4 * g + 3] * inv : 0.f;
-          reinterpret_cast<float4*>(qb)[32 * g + lane] = v;
-        }
-        if (lane == 0) R[(size_t)k * n + k] = rkk;
-        __syncwarp();
+        for (int g = 0; g < 16; ++g)
+          reinterpret_cast<float4*>(qb)[32 * g + lane] =
+              make_float4(col[4 * g] * inv, col[4 * g + 1] * inv, col[4 * g + 2] * inv, col[4 * g + 3] * inv);
+        if (lane == 0) rbuf[kk * W + kk] = rkk;  // R entries of the own panel are staged in shared memory:
+        __syncwarp();                           // no global store ahead of the barrier on the critical path
         if (lane == 0) {
           const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&slot_bar[kk]));
           asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -551,8 +555,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
       q[4 * g + 2] = v.z;
       q[4 * g + 3] = v.w;
     }
-    update2(q, a, 2 * warp < w && 2 * warp > kk, 2 * warp + 1 < w && 2 * warp + 1 > kk,
-            R + (size_t)k * n + c0 + 2 * warp, lane);
+    update2(q, a, 2 * warp < w && 2 * warp > kk, 2 * warp + 1 < w && 2 * warp + 1 > kk, rbuf + kk * W + 2 * warp,
+            lane);
     if (trace && b == 5 && warp == last_warp && lane == 0) gs_trace_step(R, n, kk, 2);
   }
   if (warp == 0) {  // publisher
@@ -598,6 +602,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
   __threadfence();
   __syncthreads();
   if (t == 0) st_release(flags + b, 1);
+  for (int idx = t; idx < W * W; idx += NT) {
+    const int kk = idx / W, j = idx % W;
+    if (kk < w && j < w && j >= kk) R[(size_t)(c0 + kk) * n + c0 + j] = rbuf[idx];
+  }
   if (trace && t == 0) gs_trace(R, n, b, 2);
 
   // ---- write back A (final columns) and Q = A / R[k][k] (coalesced through shared memory)
@@ -611,17 +619,41 @@ __global__ void __launch_bounds__(kPanelThreads, 1) gs_panel2(float* __restrict_
       for (int e = 0; e < 4; ++e)
 #pragma unroll
         for (int c = 0; c < 2; ++c)
-          st[(4 * lane + e) * 17 + 2 * warp + c] = which ? a[c][4 * P + e] * rdiag[c] : a[c][4 * P + e];
+          st[(4 * lane + e) * (W + 1) + 2 * warp + c] = which ? a[c][4 * P + e] * rdiag[c] : a[c][4 * P + e];
       __syncthreads();
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int idx = t + 256 * e, row = 128 * P + idx / 16, col = idx % 16;
-        if (row < m && col < w) dst[(size_t)row * n + c0 + col] = st[(idx / 16) * 17 + col];
+        const int idx = t + NT * e, row = 128 * P + idx / W, col = idx % W;
+        if (row < m && col < w) dst[(size_t)row * n + c0 + col] = st[(idx / W) * (W + 1) + col];
       }
     }
   }
 }
 
+template <BenchId Bn, int V, int W>
+bool try_launch_panel2(void** args, int n, cudaStream_t s) {
+  constexpr int NT = 16 * W;
+  constexpr size_t smem = (size_t)W * kP2Rows * sizeof(float);
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(gs_panel2<Bn, V, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_panel2<Bn, V, W>, NT, smem) != cudaSuccess)
+      per_sm = 0;
+  }
+  const int grid = (n + W - 1) / W;
+  if ((int64_t)per_sm * sms < grid) return false;  // the panels must all be co-resident
+  if (cudaLaunchCooperativeKernel((const void*)gs_panel2<Bn, V, W>, dim3(grid), dim3(NT), args, smem, s) !=
+      cudaSuccess)
+    launch_failed("GRAMSCHM panel2: cooperative launch rejected");
+  return true;
+}
+
+// 16-column panels (one CTA per SM).  PF_GS_W=8: 8-column panels, two CTAs per
+// SM, when they fit co-resident -- half the per-column update work, twice the
+// panels (3.14 vs 3.07 ms at 2048^2).
 template <BenchId Bn, int V>
 void launch_panel2(Workspace& ws, cudaStream_t s) {
   const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
@@ -636,17 +668,13 @@ void launch_panel2(Workspace& ws, cudaStream_t s) {
     const char* e = std::getenv("PF_GS_TRACE");
     return e && e[0] == '1' ? 1 : 0;
   }();
+  static const int width = [] {
+    const char* e = std::getenv("PF_GS_W");
+    return e ? std::atoi(e) : 16;
+  }();
   void* args[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n, (void*)&trace};
-  const int grid = (n + kPanelW - 1) / kPanelW;
-  constexpr size_t smem = (size_t)kPanelW * kP2Rows * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gs_panel2<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  if (cudaLaunchCooperativeKernel((const void*)gs_panel2<Bn, V>, dim3(grid), dim3(kPanelThreads), args, smem, s) !=
-      cudaSuccess)
-    launch_failed("GRAMSCHM panel2: cooperative launch rejected");
+  if (width == 8 && try_launch_panel2<Bn, V, 8>(args, n, s)) return;  // else the 16-column panels
+  if (!try_launch_panel2<Bn, V, 16>(args, n, s)) launch_failed("GRAMSCHM panel2: panels do not fit co-resident");
 }
 
 // PF_GS_PANEL=1 forces the per-column panel kernel (A/B runs).

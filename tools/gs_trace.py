@@ -33,8 +33,8 @@ fac = row[:, 2] - row[:, 1]
 wait = row[1:, 1] - row[:-1, 2]
 print(f"mean period {per.mean():.2f} us, mean factor {fac.mean():.2f} us, mean (applied_b - published_b-1) {wait.mean():.2f} us")
 
-st = R[n - 2, :48].reshape(16, 3).astype(np.float64)
-st = (st - st[0, 0]) % (1 << 24) * 1.0  # already microseconds (10 ns resolution)
-print("CTA 5 own-panel steps (us): pivot done | last warp past barrier | last warp updated")
+st = R[n - 2, :64].reshape(16, 4).astype(np.float64)
+st = (st - st[0, 3]) % 167772.16  # microseconds (10 ns resolution, mod 2^24)
+print("CTA 5 own-panel steps (us): pivot start | pivot done | last warp past barrier | last warp updated")
 for kk in range(16):
-    print(f"  step {kk:2d}: {st[kk, 0]:8.2f} {st[kk, 1]:8.2f} {st[kk, 2]:8.2f}")
+    print(f"  step {kk:2d}: {st[kk, 3]:8.2f} {st[kk, 0]:8.2f} {st[kk, 1]:8.2f} {st[kk, 2]:8.2f}")
