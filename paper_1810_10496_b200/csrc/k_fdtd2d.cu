@@ -178,12 +178,15 @@ __global__ void __launch_bounds__(256) step_fused4(const float* __restrict__ fic
 // cell per side (global boundary rules need no neighbours, so they do not
 // shrink).  L2 traffic per time step falls from 6 field passes to
 // ~(6 * 1.27) / kTB.
-constexpr int kTR = 64;                 // region edge (16 float4 per row)
-constexpr int kTBThreads = 256;         // 4 row-quads per thread per phase
-constexpr size_t kTBSmem = 3ull * kTR * kTR * sizeof(float);
+// kTB: time steps per launch = halo width; kTR: region edge (float4 rows);
+// output tile edge kTR - 2 kTB; kTBThreads threads, kTR^2 / 4 / kTBThreads
+// row-quads per thread per phase
+template <int kTR>
+constexpr size_t tb_smem() {
+  return 3ull * kTR * kTR * sizeof(float);
+}
 
-// kTB: time steps per launch = halo width; output tile edge kTR - 2 kTB
-template <BenchId Bn, int V, int kTB>
+template <BenchId Bn, int V, int kTB, int kTR, int kTBThreads>
 __global__ void __launch_bounds__(kTBThreads) step_tb(const float* __restrict__ fict, const float* __restrict__ ex0,
                                                       const float* __restrict__ ey0, const float* __restrict__ hz0,
                                                       float* __restrict__ ex1, float* __restrict__ ey1,
@@ -195,7 +198,7 @@ __global__ void __launch_bounds__(kTBThreads) step_tb(const float* __restrict__ 
   float* shz = sey + kTR * kTR;
   const int gi0 = blockIdx.y * kTT - kTB, gj0 = blockIdx.x * kTT - kTB;  // region origin (global)
   constexpr int kQ = kTR / 4;                                           // float4 per region row
-  constexpr int kItems = kTR * kQ / kTBThreads;                         // 4
+  constexpr int kItems = kTR * kQ / kTBThreads;
   // ---- load (ny % 4 == 0 and gj0 % 4 == 0: a float4 is all in or all out of the domain)
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
@@ -281,16 +284,17 @@ __global__ void __launch_bounds__(kTBThreads) step_tb(const float* __restrict__ 
   }
 }
 
-template <BenchId Bn, int V, int kTB>
+template <BenchId Bn, int V, int kTB, int kTR, int kTBThreads>
 void tb_sequence(Workspace& ws, cudaStream_t s) {
   constexpr int kTT = kTR - 2 * kTB;
+  constexpr size_t smem = tb_smem<kTR>();
   const int nx = (int)ws.dims.d[0], ny = (int)ws.dims.d[1], tmax = (int)ws.dims.d[2];
   const size_t n = (size_t)nx * ny;
   float* scratch = ws.ensure_scratch(3 * n * sizeof(float));
   float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(step_tb<Bn, V, kTB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTBSmem);
+    cudaFuncSetAttribute(step_tb<Bn, V, kTB, kTR, kTBThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   const dim3 grid(cdiv(ny, kTT), cdiv(nx, kTT));
@@ -298,16 +302,17 @@ void tb_sequence(Workspace& ws, cudaStream_t s) {
   for (int t = 0; t < tmax; t += kTB, ++launches) {
     float** src = buf[launches & 1];
     float** dst = buf[(launches + 1) & 1];
-    step_tb<Bn, V, kTB><<<grid, kTBThreads, kTBSmem, s>>>(ws.a.p[0], src[0], src[1], src[2], dst[0], dst[1], dst[2],
-                                                         nx, ny, t, std::min(kTB, tmax - t));
+    step_tb<Bn, V, kTB, kTR, kTBThreads><<<grid, kTBThreads, smem, s>>>(
+        ws.a.p[0], src[0], src[1], src[2], dst[0], dst[1], dst[2], nx, ny, t, std::min(kTB, tmax - t));
   }
   if (launches & 1)
     for (int f = 0; f < 3; ++f) cudaMemcpyAsync(buf[0][f], buf[1][f], n * sizeof(float), cudaMemcpyDeviceToDevice, s);
 }
 
-// Stage-2 time steps per launch: 4 by default (2048^2 x 500: 5.77 ms vs 6.16
-// ms for the per-step fused sequence); PF_FDTD_TB=0 selects the per-step
-// sequence, PF_FDTD_TB=8 a deeper blocking (6.47 ms; A/B runs).
+// Stage-2 time steps per launch: 4 by default on 64x64 regions (2048^2 x 500:
+// 5.77 ms vs 6.16 ms for the per-step fused sequence); PF_FDTD_TB=0 selects the
+// per-step sequence, PF_FDTD_TB=8 a deeper blocking (6.47 ms; A/B runs).  128x128
+// regions (one 512-thread CTA per SM) measured 6.5-7.7 ms for 4-16 steps.
 inline int fdtd_tb_depth() {
   static const int d = [] {
     const char* e = std::getenv("PF_FDTD_TB");
@@ -363,8 +368,8 @@ struct Run {
       const bool tb = ny % 4 == 0 && !fdtd_tb_disabled();
       const int d = fdtd_tb_depth();
       cudaGraphExec_t g = !tb      ? cached_graph(ws, V + 1000, &fused_sequence<B_FDTD2D, V>)
-                          : d == 8 ? cached_graph(ws, V + 3000, &tb_sequence<B_FDTD2D, V, 8>)
-                                   : cached_graph(ws, V, &tb_sequence<B_FDTD2D, V, 4>);
+                          : d == 8 ? cached_graph(ws, V + 3000, &tb_sequence<B_FDTD2D, V, 8, 64, 256>)
+                                   : cached_graph(ws, V, &tb_sequence<B_FDTD2D, V, 4, 64, 256>);
       cudaGraphLaunch(g, s);
     }
   }
