@@ -1,13 +1,18 @@
-# ncu evidence for profiles/ (never a bench number: ncu serialises and replays)
+# ncu evidence for profiles/ (never a bench number: ncu serialises and replays).
+# Launch list of the bench step + one --set full capture per dominant kernel;
+# summarise with: python tools/ncu_summary.py gpurun_out/prof profiles/<name>.md
 set -x
-mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+mkdir -p gpurun_out/prof
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv \
     python bench.py --steps 2 --warmup 3 --e2e-steps 0 --cpu-evals 0 --num-sequences 200 > gpurun_out/bench_under_ncu.log 2>&1
-for spec in "ATAX 16384,16384 stage=2 s2_fused" "BICG 16384,16384 stage=2 s2_fused" \
-            "GESUMMV 16384 stage=2 gesummv_s2" "2MM 2048,2048,2048,2048 stage=2 tc_gemm_kernel" \
-            "3DCONV 256,256,256 stage=1 conv3d_s1" "FDTD-2D 2048,2048,20 stage=1 step_fused"; do
+for spec in "ATAX 16384,16384 stage=2 s2_fused" "GESUMMV 16384 stage=2 gesummv_s2" \
+            "2MM 2048,2048,2048,2048 stage=2 tc_tma2_kernel" "3DCONV 256,256,256 stage=2 conv3d_s2d" \
+            "2DCONV 4096,4096 stage=2 conv2d_s2" "FDTD-2D 2048,2048,20 stage=2 step_tb" "GEMM 512,512,512 stage=2 tc_tma_kernel" \
+            "SYRK 2048,2048 stage=2 tc_tma2_kernel" "CORR 2048,2048 stage=2 tc_tma2_kernel"; do
   set -- $spec
-  ncu --set full --clock-control none --import-source on -k regex:$4 -s 1 -c 1 \
-      -o gpurun_out/prof_$1_$4 python tools/profile_kernels.py $1 $2 $3 3 > gpurun_out/prof_$1_$4.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$4 -s 1 -c 1 \
+      -o gpurun_out/prof/prof_$1_$4 python tools/profile_kernels.py $1 $2 $3 3 > gpurun_out/prof/prof_$1.log 2>&1
 done
-ls -la gpurun_out
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gs_panel2 -c 1 \
+   -o gpurun_out/prof/prof_GRAMSCHM_gs_panel2 python tools/profile_kernels.py GRAMSCHM 2048,2048 stage=2,vec=1 1 > /dev/null 2>&1
+ls -la gpurun_out/prof
