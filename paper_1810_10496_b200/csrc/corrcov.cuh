@@ -125,19 +125,23 @@ __global__ void __launch_bounds__(256) colsum_split(const float* __restrict__ da
   const int i0 = 1 + blockIdx.y * rows_per_split;
   const int i1 = min(n + 1, i0 + rows_per_split);
   const float mu = kPass ? mean[j] : 0.f;
-  float s0 = 0.f, s1 = 0.f;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // four loads in flight per thread
   int i = i0;
-  for (; i + 1 < i1; i += 2) {
+  for (; i + 3 < i1; i += 4) {
     const float a = __ldg(data + (size_t)i * (m + 1) + j) - mu;
     const float b = __ldg(data + (size_t)(i + 1) * (m + 1) + j) - mu;
+    const float c = __ldg(data + (size_t)(i + 2) * (m + 1) + j) - mu;
+    const float d = __ldg(data + (size_t)(i + 3) * (m + 1) + j) - mu;
     s0 += kPass ? a * a : a;
     s1 += kPass ? b * b : b;
+    s2 += kPass ? c * c : c;
+    s3 += kPass ? d * d : d;
   }
-  if (i < i1) {
+  for (; i < i1; ++i) {
     const float a = __ldg(data + (size_t)i * (m + 1) + j) - mu;
     s0 += kPass ? a * a : a;
   }
-  atomicAdd(out + j, s0 + s1);
+  atomicAdd(out + j, (s0 + s1) + (s2 + s3));
 }
 
 template <BenchId Bn, int V, int kPass>
@@ -169,60 +173,87 @@ inline void launch_colstat(const float* data, const float* mean, float* out, int
 }
 
 // Stage 2: normalise in place (reduce_s0's arithmetic) and write the result
-// transposed: xt[(j-1) * ldx + i-1] = data[i][j].  Block (32, 8), 32x32 tile.
+// transposed: xt[(j-1) * ldx + i-1] = data[i][j].  Block (32, 8) on a 64x64
+// tile: 16 elements per thread, all loads issued before the first store.
+constexpr int kCT = 64;
+
 template <BenchId Bn, int V, bool kCorr>
 __global__ void __launch_bounds__(256) reduce_transpose(const float* __restrict__ mean, const float* __restrict__ stdv,
                                                         float* data, float* __restrict__ xt, int m, int n,
                                                         int ldx) {
-  __shared__ float t[32][33];
-  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  __shared__ float t[kCT][kCT + 1];
+  const int j0 = blockIdx.x * kCT, i0 = blockIdx.y * kCT;
+  float mu[2], sc[2];
 #pragma unroll
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const int i = i0 + r + 1, j = j0 + threadIdx.x + 1;
-    if (i <= n && j <= m) {
-      float* p = data + (size_t)i * (m + 1) + j;
-      float v = *p - mean[j];
-      if constexpr (kCorr) v /= (sqrtf(kFloatN) * stdv[j]);
-      *p = v;
-      t[r][threadIdx.x] = v;
-    }
+  for (int c = 0; c < 2; ++c) {
+    const int j = j0 + threadIdx.x + 32 * c + 1;
+    mu[c] = j <= m ? mean[j] : 0.f;
+    sc[c] = kCorr && j <= m ? sqrtf(kFloatN) * stdv[j] : 1.f;
   }
+  float v[kCT / 8][2];
+#pragma unroll
+  for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int i = i0 + threadIdx.y + 8 * q + 1, j = j0 + threadIdx.x + 32 * c + 1;
+      v[q][c] = (i <= n && j <= m) ? data[(size_t)i * (m + 1) + j] : 0.f;
+    }
+#pragma unroll
+  for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int r = threadIdx.y + 8 * q, i = i0 + r + 1, j = j0 + threadIdx.x + 32 * c + 1;
+      if (i <= n && j <= m) {
+        float x = v[q][c] - mu[c];
+        if constexpr (kCorr) x /= sc[c];
+        data[(size_t)i * (m + 1) + j] = x;
+        t[r][threadIdx.x + 32 * c] = x;
+      }
+    }
   __syncthreads();
 #pragma unroll
-  for (int r = threadIdx.y; r < 32; r += 8) {
-    const int j = j0 + r, i = i0 + threadIdx.x;
-    if (j < m && i < n) xt[(size_t)j * ldx + i] = t[threadIdx.x][r];
-  }
+  for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int j = j0 + threadIdx.y + 8 * q, i = i0 + threadIdx.x + 32 * c;
+      if (j < m && i < n) xt[(size_t)j * ldx + i] = t[threadIdx.x + 32 * c][threadIdx.y + 8 * q];
+    }
 }
 
-// symmat[1 + r][1 + c] = G[min(r,c)][max(r,c)] (pitch ldg) (only G's upper triangle is
-// computed); CORR's diagonal is 1.  Block (32, 8), 32x32 tile.
+// symmat[1 + r][1 + c] = G[min(r,c)][max(r,c)] (pitch ldg) (only G's upper
+// triangle is computed); CORR's diagonal is 1.  Block (32, 8), 64x64 tile.
 template <BenchId Bn, int V, bool kCorr>
 __global__ void __launch_bounds__(256) sym_scatter(const float* __restrict__ G, int ldg, float* sym, int m) {
-  __shared__ float t[32][33];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  __shared__ float t[kCT][kCT + 1];
+  const int c0 = blockIdx.x * kCT, r0 = blockIdx.y * kCT;
   const bool lower = r0 > c0;  // tile strictly below the diagonal blocks: read the transposed tile
 #pragma unroll
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int gr = (lower ? c0 : r0) + k, gc = (lower ? r0 : c0) + threadIdx.x;
-    if (gr < m && gc < m) t[k][threadIdx.x] = G[(size_t)gr * ldg + gc];
-  }
+  for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int k = threadIdx.y + 8 * q, x = threadIdx.x + 32 * c;
+      const int gr = (lower ? c0 : r0) + k, gc = (lower ? r0 : c0) + x;
+      if (gr < m && gc < m) t[k][x] = G[(size_t)gr * ldg + gc];
+    }
   __syncthreads();
 #pragma unroll
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int r = r0 + k, c = c0 + threadIdx.x;
-    if (r < m && c < m) {
-      float v;
-      if (lower)
-        v = t[threadIdx.x][k];
-      else if (r <= c)
-        v = t[k][threadIdx.x];
-      else
-        v = t[threadIdx.x][k];  // diagonal tile, lower half: mirror within the tile
-      if (kCorr && r == c) v = 1.0f;
-      sym[(size_t)(r + 1) * (m + 1) + (c + 1)] = v;
+  for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int k = threadIdx.y + 8 * q, x = threadIdx.x + 32 * c;
+      const int r = r0 + k, col = c0 + x;
+      if (r < m && col < m) {
+        float v;
+        if (lower)
+          v = t[x][k];
+        else if (r <= col)
+          v = t[k][x];
+        else
+          v = t[x][k];  // diagonal tile, lower half: mirror within the tile
+        if (kCorr && r == col) v = 1.0f;
+        sym[(size_t)(r + 1) * (m + 1) + (col + 1)] = v;
+      }
     }
-  }
 }
 
 // One variant run.  arrays: data, mean, [std,] symmat
@@ -246,7 +277,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
       const int np = (n + 3) / 4 * 4, mp = (m + 3) / 4 * 4;
       float* xt = ws.ensure_scratch(((size_t)m * np + (size_t)m * mp) * sizeof(float));
       float* G = xt + (size_t)m * np;
-      reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, 32), cdiv(n, 32)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt, m,
+      reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt, m,
                                                                                            n, np);
       TcGemmArgs g{m, m, n, 1.f, 0.f, xt, np, false, xt, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
       g.tile_flags = ws.ensure_tile_flags();
@@ -255,7 +286,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
         launch_failed("CORR/COVAR stage 2: TMA operand maps rejected");
         return;
       }
-      sym_scatter<Bn, V, kCorr><<<dim3(cdiv(m, 32), cdiv(m, 32)), dim3(32, 8), 0, s>>>(G, mp, sym, m);
+      sym_scatter<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(m, kCT)), dim3(32, 8), 0, s>>>(G, mp, sym, m);
       return;
     }
     reduce_s0<Bn, V, kCorr><<<dim3(cdiv(m, kBX), cdiv(n, kBY)), dim3(kBX, kBY), 0, s>>>(mean, stdv, data, m, n);

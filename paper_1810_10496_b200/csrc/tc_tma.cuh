@@ -750,8 +750,13 @@ inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair, bool uppe
     for (int64_t i = 0; i < bm; ++i) tiles += std::max<int64_t>(0, bn - i);
   }
   const int64_t ctas = pair ? 2 * tiles : tiles;
+  static const int cap = [] {  // PF_TC_SPLITS=<n>: cap the split factor (A/B runs)
+    const char* e = std::getenv("PF_TC_SPLITS");
+    return e ? std::max(1, std::atoi(e)) : 1 << 30;
+  }();
   int splits = 1;
   if (ctas < 74) splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / ctas, kblocks / 2));
+  splits = std::min(splits, cap);
   const int per = (kblocks + splits - 1) / splits;
   return (kblocks + per - 1) / per;
 }
