@@ -630,216 +630,6 @@ __global__ void __launch_bounds__(16 * W, 1) gs_panel2(float* __restrict__ A, fl
   }
 }
 
-// ---- stage 2, vec=1, row-slice form (gs_panel3, m <= 2048).  CTA b owns
-// columns [16b, 16b+16) like gs_panel2, but warp w holds ROWS 256w .. 256w+255
-// of all 16 columns (lane: rows 256w + lane + 32t, t < 8): every MGS step is
-// shared by the eight warps -- per-warp partial dots (8 FMAs per column),
-// a 16-shuffle reduce-scatter, one block barrier, the eight partials summed in
-// fixed order -- and no warp ever runs alone (no single-warp pivot).  A ninth
-// warp publishes each q column (device fence + release flag) off the critical
-// path; q slices come straight from L2 into registers (1 KB per warp per q).
-constexpr int kP3Threads = 288;  // 8 compute warps + 1 publisher warp
-
-__device__ __forceinline__ void p3_barrier() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-// r_c = q . a_c over the CTA for all 16 columns; a_c -= r_c q for cfrom <= c < w.
-// R[k][c0 + c] written by warp 0.  part: this step's [8][16] partial buffer.
-__device__ __forceinline__ void p3_mgs(float (&a)[16][8], const float (&q)[8], float (*part)[16], int cfrom, int w,
-                                       float* rrow, int lane, int warp) {
-  float s[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    float x = 0.f;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) x = fmaf(q[t], a[c][t], x);
-    s[c] = x;
-  }
-  // reduce-scatter over the 32 lanes: lane ends with column (lane >> 1) & 15
-#pragma unroll
-  for (int h = 8; h >= 1; h >>= 1) {
-    const bool up = lane & (2 * h);
-#pragma unroll
-    for (int i = 0; i < h; ++i) {
-      const float mine = up ? s[i + h] : s[i];
-      const float other = up ? s[i] : s[i + h];
-      s[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2 * h);
-    }
-  }
-  s[0] += __shfl_xor_sync(0xffffffffu, s[0], 1);
-  if (!(lane & 1)) part[warp][(lane >> 1) & 15] = s[0];
-  p3_barrier();
-  float tot = 0.f;
-  if (lane < 16) {
-#pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) tot += part[w2][lane];
-  }
-  if (warp == 0 && lane >= cfrom && lane < w) rrow[lane] = tot;
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    float r = __shfl_sync(0xffffffffu, tot, c);
-    r = (c >= cfrom && c < w) ? r : 0.f;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) a[c][t] = fmaf(-q[t], r, a[c][t]);
-  }
-}
-
-__device__ __forceinline__ void p3_load_q(float (&q)[8], const float* __restrict__ col, int warp, int lane) {
-#pragma unroll
-  for (int t = 0; t < 8; ++t) q[t] = __ldcg(col + 256 * warp + lane + 32 * t);
-}
-
-template <BenchId Bn, int V>
-__global__ void __launch_bounds__(kP3Threads, 1) gs_panel3(float* __restrict__ A, float* __restrict__ R,
-                                                           float* __restrict__ Q, float* __restrict__ qbuf,
-                                                           int* __restrict__ flags, int m, int n) {
-  __shared__ float part[2][8][16];
-  __shared__ float npart[2][8];
-  __shared__ __align__(8) uint64_t pub_bar[16];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int b = blockIdx.x, c0 = b * 16, w = min(16, n - c0);
-  int* colflags = flags + n;
-  if (t < 16) {
-    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&pub_bar[t]));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(bar) : "memory");
-  }
-  __syncthreads();
-  if (warp == 8) {  // publisher
-    for (int kk = 0; kk < w; ++kk) {
-      const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&pub_bar[kk]));
-      uint32_t ok = 0;
-      while (!ok)
-        asm volatile(
-            "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], 0;\n\t"
-            "selp.b32 %0, 1, 0, P;\n\t}"
-            : "=r"(ok)
-            : "r"(bar)
-            : "memory");
-      if (lane == 0) {
-        __threadfence();
-        st_release(colflags + c0 + kk, 1);
-      }
-    }
-    if (lane == 0) {
-      __threadfence();
-      st_release(flags + b, 1);
-    }
-    return;
-  }
-
-  // ---- load the panel: lane rows 256 warp + lane + 32 t
-  float a[16][8];
-#pragma unroll
-  for (int tt = 0; tt < 8; ++tt) {
-    const int row = 256 * warp + lane + 32 * tt;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) a[c][tt] = (row < m && c < w) ? A[(size_t)row * n + c0 + c] : 0.f;
-  }
-  int pbuf = 0;
-
-  // ---- apply earlier panels (the one just before is consumed column by column)
-  for (int pb = 0; pb < b; ++pb) {
-    if (pb < b - 1) {
-      if (t == 0)
-        while (ld_acquire(flags + pb) == 0) {
-        }
-      p3_barrier();
-    }
-    float q[8], qn[8];
-    if (pb == b - 1) {
-      if (t == 0)
-        while (ld_acquire(colflags + pb * 16) == 0) {
-        }
-      p3_barrier();
-    }
-    p3_load_q(q, qbuf + (size_t)(pb * 16) * kP2Rows, warp, lane);
-    for (int kk = 0; kk < 16; ++kk) {
-      const int k = pb * 16 + kk;
-      if (kk + 1 < 16) {
-        if (pb == b - 1) {
-          if (t == 0)
-            while (ld_acquire(colflags + k + 1) == 0) {
-            }
-          p3_barrier();
-        }
-        p3_load_q(qn, qbuf + (size_t)(k + 1) * kP2Rows, warp, lane);  // prefetch the next q
-      }
-      p3_mgs(a, q, part[pbuf], 0, w, R + (size_t)k * n + c0, lane, warp);
-      pbuf ^= 1;
-#pragma unroll
-      for (int tt = 0; tt < 8; ++tt) q[tt] = qn[tt];
-    }
-  }
-
-  // ---- factor the own panel (unrolled: the pivot column index is static)
-  float rinv[16];
-#pragma unroll
-  for (int kk = 0; kk < 16; ++kk) {
-    rinv[kk] = 1.f;
-    if (kk >= w) continue;
-    const int k = c0 + kk;
-    float sq = 0.f;
-#pragma unroll
-    for (int tt = 0; tt < 8; ++tt) sq = fmaf(a[kk][tt], a[kk][tt], sq);
-    sq = warp_sum(sq);
-    if (lane == 0) npart[kk & 1][warp] = sq;
-    p3_barrier();
-    float nrm = 0.f;
-#pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) nrm += npart[kk & 1][w2];
-    const float inv = rsqrtf(nrm);
-    rinv[kk] = inv;
-    if (warp == 0 && lane == 0) R[(size_t)k * n + k] = nrm * inv;
-    float q[8];
-    float* qg = qbuf + (size_t)k * kP2Rows + 256 * warp + lane;
-#pragma unroll
-    for (int tt = 0; tt < 8; ++tt) {
-      q[tt] = a[kk][tt] * inv;
-      qg[32 * tt] = q[tt];
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&pub_bar[kk]));
-      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-    }
-    if (kk + 1 < w) {
-      p3_mgs(a, q, part[pbuf], kk + 1, w, R + (size_t)k * n + c0, lane, warp);
-      pbuf ^= 1;
-    }
-  }
-
-  // ---- write back A (final columns) and Q = A / R[k][k]
-#pragma unroll
-  for (int tt = 0; tt < 8; ++tt) {
-    const int row = 256 * warp + lane + 32 * tt;
-    if (row >= m) continue;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      if (c < w) {
-        A[(size_t)row * n + c0 + c] = a[c][tt];
-        Q[(size_t)row * n + c0 + c] = a[c][tt] * rinv[c];
-      }
-    }
-  }
-}
-
-template <BenchId Bn, int V>
-bool try_launch_panel3(void** args, int n, cudaStream_t s) {
-  static int per_sm = -1, sms = 0;
-  if (per_sm < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_panel3<Bn, V>, kP3Threads, 0) != cudaSuccess)
-      per_sm = 0;
-  }
-  const int grid = (n + 15) / 16;
-  if ((int64_t)per_sm * sms < grid) return false;
-  if (cudaLaunchCooperativeKernel((const void*)gs_panel3<Bn, V>, dim3(grid), dim3(kP3Threads), args, 0, s) !=
-      cudaSuccess)
-    launch_failed("GRAMSCHM panel3: cooperative launch rejected");
-  return true;
-}
-
 template <BenchId Bn, int V, int W>
 bool try_launch_panel2(void** args, int n, cudaStream_t s) {
   constexpr int NT = 16 * W;
@@ -863,7 +653,9 @@ bool try_launch_panel2(void** args, int n, cudaStream_t s) {
 
 // 16-column panels (one CTA per SM).  PF_GS_W=8: 8-column panels, two CTAs per
 // SM, when they fit co-resident -- half the per-column update work, twice the
-// panels (3.14 vs 3.07 ms at 2048^2).
+// panels (3.14 vs 3.07 ms at 2048^2).  Also measured and dropped: a row-slice
+// layout (warp = 256 rows of all 16 columns, every MGS step shared by the 8
+// warps through a reduce-scatter and one block barrier): 4.69 ms.
 template <BenchId Bn, int V>
 void launch_panel2(Workspace& ws, cudaStream_t s) {
   const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
@@ -882,10 +674,6 @@ void launch_panel2(Workspace& ws, cudaStream_t s) {
     const char* e = std::getenv("PF_GS_W");
     return e ? std::atoi(e) : 16;
   }();
-  if (width == 3) {  // PF_GS_W=3: the row-slice panel kernel (A/B runs)
-    void* args3[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n};
-    if (try_launch_panel3<Bn, V>(args3, n, s)) return;
-  }
   void* args[] = {&A, &R, &Q, &qbuf, &flags, (void*)&m, (void*)&n, (void*)&trace};
   if (width == 8 && try_launch_panel2<Bn, V, 8>(args, n, s)) return;  // else the 16-column panels
   if (!try_launch_panel2<Bn, V, 16>(args, n, s)) launch_failed("GRAMSCHM panel2: panels do not fit co-resident");
