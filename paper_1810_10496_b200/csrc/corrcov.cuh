@@ -9,8 +9,9 @@
 // stage 1  row-split column statistics (atomics) and the Gram matrix D^T D
 //          as an upper-triangle tiled SIMT GEMM + mirror.
 // stage 2  the normalisation pass also writes the centred (scaled) data
-//          transposed into an aligned m x n scratch (32x32 shared-memory
-//          tiles), so the Gram matrix X X^T runs on the TMA-fed tcgen05
+//          transposed into an aligned m x n scratch (64x64 shared-memory
+//          tiles), with its 3xTF32 lo image, so the Gram matrix X X^T runs
+//          pre-split on the TMA-fed tcgen05
 //          3xTF32 kernel exactly like SYRK (upper-triangle tiles, K-major
 //          operands, TMA epilogue into an aligned m x m scratch); one tiled
 //          pass then scatters it into the 1-based symmat with the mirror (and
@@ -179,8 +180,8 @@ constexpr int kCT = 64;
 
 template <BenchId Bn, int V, bool kCorr>
 __global__ void __launch_bounds__(256) reduce_transpose(const float* __restrict__ mean, const float* __restrict__ stdv,
-                                                        float* data, float* __restrict__ xt, int m, int n,
-                                                        int ldx) {
+                                                        float* data, float* __restrict__ xt,
+                                                        float* __restrict__ xt_lo, int m, int n, int ldx) {
   __shared__ float t[kCT][kCT + 1];
   const int j0 = blockIdx.x * kCT, i0 = blockIdx.y * kCT;
   float mu[2], sc[2];
@@ -216,7 +217,11 @@ __global__ void __launch_bounds__(256) reduce_transpose(const float* __restrict_
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int j = j0 + threadIdx.y + 8 * q, i = i0 + threadIdx.x + 32 * c;
-      if (j < m && i < n) xt[(size_t)j * ldx + i] = t[threadIdx.x + 32 * c][threadIdx.y + 8 * q];
+      if (j < m && i < n) {
+        const float x = t[threadIdx.x + 32 * c][threadIdx.y + 8 * q];
+        xt[(size_t)j * ldx + i] = x;
+        xt_lo[(size_t)j * ldx + i] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);  // 3xTF32 lo image
+      }
     }
 }
 
@@ -275,11 +280,16 @@ inline void run(Workspace& ws, cudaStream_t s) {
     if constexpr (kStage == 2) {
       // 16-byte pitches for the TMA maps (K tail beyond n reads as zero)
       const int np = (n + 3) / 4 * 4, mp = (m + 3) / 4 * 4;
-      float* xt = ws.ensure_scratch(((size_t)m * np + (size_t)m * mp) * sizeof(float));
-      float* G = xt + (size_t)m * np;
-      reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt, m,
-                                                                                           n, np);
+      float* xt = ws.ensure_scratch((2 * (size_t)m * np + (size_t)m * mp) * sizeof(float));
+      float* xt_lo = xt + (size_t)m * np;
+      float* G = xt_lo + (size_t)m * np;
+      reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt,
+                                                                                           xt_lo, m, n, np);
+      // the transpose also writes the lo image, so the Gram runs pre-split
+      // (no converter warps) at no extra pass
       TcGemmArgs g{m, m, n, 1.f, 0.f, xt, np, false, xt, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
+      g.Alo = xt_lo;
+      g.Blo = xt_lo;
       g.tile_flags = ws.ensure_tile_flags();
       g.epoch = ++ws.tile_epoch;
       if (!launch_tc_tma<Bn, V>(g, s)) {
