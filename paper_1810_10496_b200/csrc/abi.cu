@@ -186,6 +186,16 @@ int* Workspace::ensure_tile_flags() {
   return tile_flags;
 }
 
+float* Workspace::ensure_aux(size_t bytes) {
+  if (aux_bytes >= bytes) return aux;
+  if (aux) cudaFree(aux);
+  aux = nullptr;
+  aux_bytes = 0;
+  if (cudaMalloc(&aux, bytes) != cudaSuccess) return nullptr;
+  aux_bytes = bytes;
+  return aux;
+}
+
 float* Workspace::ensure_scratch(size_t bytes) {
   if (scratch_bytes >= bytes) return scratch;
   if (scratch) cudaFree(scratch);
@@ -390,6 +400,7 @@ int pf_ws_destroy(pf_ws* ws) {
   }
   if (ws->scratch) cudaFree(ws->scratch);
   if (ws->tile_flags) cudaFree(ws->tile_flags);
+  if (ws->aux) cudaFree(ws->aux);
   if (ws->graphs) {
     auto* gc = static_cast<GraphCache*>(ws->graphs);
     for (auto& kv : gc->exec) cudaGraphExecDestroy(kv.second);

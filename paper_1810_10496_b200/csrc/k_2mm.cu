@@ -53,10 +53,15 @@ struct Run {
       launch_simt_gemm<B_2MM, V, false, false, false>(
           SimtGemmArgs{ni, nl, nj, 1.f, 0.f, C, nj, D, nl, nullptr, nullptr, nullptr, nl, E, nl, 0}, s);
     } else {
-      launch_contraction<B_2MM, V>(
-          ws, TcGemmArgs{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr, nullptr, nj, C, nj, 0}, s);
-      launch_contraction<B_2MM, V>(
-          ws, TcGemmArgs{ni, nl, nj, 1.f, 0.f, C, nj, false, D, nl, false, nullptr, nullptr, nullptr, nl, E, nl, 0}, s);
+      // C's lo image comes out of the first product's epilogue (when it runs
+      // pre-split, without split-K), so the second product splits only D
+      float* clo = ws.ensure_aux((size_t)ni * nj * sizeof(float));
+      TcGemmArgs p1{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr, nullptr, nj, C, nj, 0};
+      p1.Dlo = clo;
+      const bool have_clo = launch_contraction<B_2MM, V>(ws, p1, s);
+      TcGemmArgs p2{ni, nl, nj, 1.f, 0.f, C, nj, false, D, nl, false, nullptr, nullptr, nullptr, nl, E, nl, 0};
+      if (have_clo) p2.Alo = clo;
+      launch_contraction<B_2MM, V>(ws, p2, s);
     }
   }
 };
@@ -71,7 +76,7 @@ int64_t elems(int a, const Dims& d) {
 int64_t launches(int v, const Dims& d) {
   if (kTab.v[v].stage != 2) return 2;
   return tc_launches(d.d[0], d.d[1], d.d[2], tma_ok(d.d[2], d.d[1])) +
-         tc_launches(d.d[0], d.d[3], d.d[1], tma_ok(d.d[1], d.d[3]));
+         tc_launches(d.d[0], d.d[3], d.d[1], tma_ok(d.d[1], d.d[3]), false, 1);  // C's lo from the first epilogue
 }
 double alg_bytes(const Dims& d) {
   const double ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3];

@@ -59,12 +59,20 @@ struct Run {
       launch_simt_gemm<B_3MM, V, false, false, false>(
           SimtGemmArgs{ni, nl, nj, 1.f, 0.f, E, nj, F, nl, nullptr, nullptr, nullptr, nl, G, nl, 0}, s);
     } else {
-      launch_contraction<B_3MM, V>(ws, TcGemmArgs{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr,
-                                              nullptr, nj, E, nj, 0}, s);
-      launch_contraction<B_3MM, V>(ws, TcGemmArgs{nj, nl, nm, 1.f, 0.f, C, nm, false, D, nl, false, nullptr, nullptr,
-                                              nullptr, nl, F, nl, 0}, s);
-      launch_contraction<B_3MM, V>(ws, TcGemmArgs{ni, nl, nj, 1.f, 0.f, E, nj, false, F, nl, false, nullptr, nullptr,
-                                              nullptr, nl, G, nl, 0}, s);
+      // E's and F's lo images come out of their products' epilogues (when
+      // those run pre-split), so G = E F needs no split pass of its own
+      float* elo = ws.ensure_aux(((size_t)ni * nj + (size_t)nj * nl) * sizeof(float));
+      float* flo = elo + (size_t)ni * nj;
+      TcGemmArgs p1{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr, nullptr, nj, E, nj, 0};
+      p1.Dlo = elo;
+      const bool have_elo = launch_contraction<B_3MM, V>(ws, p1, s);
+      TcGemmArgs p2{nj, nl, nm, 1.f, 0.f, C, nm, false, D, nl, false, nullptr, nullptr, nullptr, nl, F, nl, 0};
+      p2.Dlo = flo;
+      const bool have_flo = launch_contraction<B_3MM, V>(ws, p2, s);
+      TcGemmArgs p3{ni, nl, nj, 1.f, 0.f, E, nj, false, F, nl, false, nullptr, nullptr, nullptr, nl, G, nl, 0};
+      if (have_elo) p3.Alo = elo;
+      if (have_flo) p3.Blo = flo;
+      launch_contraction<B_3MM, V>(ws, p3, s);
     }
   }
 };
@@ -80,7 +88,7 @@ int64_t launches(int v, const Dims& d) {
   if (kTab.v[v].stage != 2) return 3;
   const int64_t ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3], nm = d.d[4];
   return tc_launches(ni, nj, nk, tma_ok(nk, nj)) + tc_launches(nj, nl, nm, tma_ok(nm, nl)) +
-         tc_launches(ni, nl, nj, tma_ok(nj, nl));
+         tc_launches(ni, nl, nj, tma_ok(nj, nl), false, 0);  // E's and F's lo from the earlier epilogues
 }
 double alg_bytes(const Dims& d) {
   const double ni = d.d[0], nj = d.d[1], nk = d.d[2], nl = d.d[3], nm = d.d[4];

@@ -109,6 +109,12 @@ struct Workspace {
   int* tile_flags;
   int tile_epoch;
   int* ensure_tile_flags();  // defined in abi.cu
+  // second lazily grown buffer for data a variant hands from one launch to a
+  // later one while the first scratch is reused in between (3xTF32 lo images
+  // of chained products)
+  float* aux;
+  size_t aux_bytes;
+  float* ensure_aux(size_t bytes);  // defined in abi.cu
 };
 constexpr int kTileFlags = 4096;
 

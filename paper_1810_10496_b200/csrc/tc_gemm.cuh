@@ -55,6 +55,9 @@ struct TcGemmArgs {
   // epoch; nullptr: split-K products use a beta pre-pass instead
   int* tile_flags = nullptr;
   int epoch = 0;
+  // optional: the epilogue also writes lo = D - trunc_tf32(D) here (pitch ldd)
+  // for a later product that consumes D as an operand
+  float* Dlo = nullptr;
 };
 
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;

@@ -47,6 +47,8 @@ struct TmaParams {
   int presplit;
   CUtensorMap tc, td;            // epilogue: Cin / D as 32x32 SWIZZLE_128B boxes (valid iff tma_epi)
   int tma_epi;
+  CUtensorMap tdl;               // lo image of D (valid iff dlo)
+  int dlo;
   int* tile_flags;               // ordered split-K: split 0 stores, the others add after its flag
   int epoch;
   int creduce;                   // split-K partials reduced across the z-cluster through DSMEM (tc_tma_kernel)
@@ -139,11 +141,13 @@ __device__ __forceinline__ void reduce_add_2d(const CUtensorMap* map, uint32_t s
 // 1024-byte aligned, ncols / 32 * 4 KB; bar: this warp's mbarrier (phase 0).
 __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr, int ncols, int row0, int col0,
                                              bool split, uint8_t* buf, uint32_t bar, int lane,
-                                             bool writes_done = false) {
+                                             bool writes_done = false, uint8_t* lobuf = nullptr) {
   if (row0 >= p.M) return;  // warp-uniform
   const int nch = min(ncols / 32, (p.N - col0 + 31) / 32);
   const bool use_c = !split && p.beta != 0.f;
+  const bool want_lo = p.dlo && !split && lobuf != nullptr;  // 4 x 4 KB ring of lo chunks
   const uint32_t sbuf = tc::smem_u32(buf);
+  const uint32_t slo = want_lo ? tc::smem_u32(lobuf) : 0u;
   if (use_c && lane == 0) {
     tc::mbar_expect_tx(bar, (uint32_t)nch * 4096u);
     for (int c = 0; c < nch; ++c) load_2d(sbuf + c * 4096, &p.tc, col0 + c * 32, row0, bar);
@@ -165,6 +169,15 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr,
                         fmaf(p.beta, ci.w, v.w));
       }
       *slot = v;
+      if (want_lo) {
+        if (j == 0 && c >= 4) {  // lo slot c % 4 is free once chunk c - 4's stores have read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+          __syncwarp();
+        }
+        float4* lslot = reinterpret_cast<float4*>(lobuf + (c & 3) * 4096 + lane * 128) + (j ^ (lane & 7));
+        *lslot = make_float4(v.x - trunc_tf32(v.x), v.y - trunc_tf32(v.y), v.z - trunc_tf32(v.z),
+                             v.w - trunc_tf32(v.w));
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
@@ -173,6 +186,7 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr,
         reduce_add_2d(&p.td, sbuf + c * 4096, col0 + c * 32, row0);
       else
         store_2d(&p.td, sbuf + c * 4096, col0 + c * 32, row0);
+      if (want_lo) store_2d(&p.tdl, slo + (c & 3) * 4096, col0 + c * 32, row0);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
@@ -428,7 +442,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
       tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
-                        tc::smem_u32(&epi_bar[quad]), lane, ordered);
+                        tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
@@ -644,7 +658,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
       tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
-                        tc::smem_u32(&epi_bar[quad]), lane, ordered);
+                        tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
@@ -779,7 +793,8 @@ inline int tc_cluster_splits(int64_t m, int64_t n, int kblocks) {
 }
 
 template <BenchId Bn, int V>
-inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
+inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written = nullptr) {
+  if (dlo_written) *dlo_written = false;
   TmaParams p;
   std::memset(&p, 0, sizeof(p));
   p.mn_lbo = tma_probe().lbo;
@@ -833,6 +848,11 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s) {
   const bool pair = !p.creduce && tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
   const int zs = p.creduce ? cz : tc_tma_splits(a.M, a.N, kblocks, pair, up);
   const int per = (kblocks + zs - 1) / zs;
+  p.dlo = (a.Dlo && p.tma_epi && zs == 1 && !p.creduce && reinterpret_cast<uintptr_t>(a.Dlo) % 16 == 0 &&
+           tma::make_map(&p.tdl, a.Dlo, a.N, a.M, a.ldd, 32, 32, false))
+              ? 1
+              : 0;
+  if (dlo_written) *dlo_written = p.dlo != 0;
   const int64_t grid_tiles = pair ? 2 * cdiv(a.N, 256) * (int64_t)cdiv(a.M, 256) : (int64_t)cdiv(a.N, 128) * cdiv(a.M, 128);
   // ordered hand-over only where the alternative pre-pass is a memset (beta
   // == 0): with beta != 0 split 0's Cin load + store serialise the splits
@@ -976,48 +996,54 @@ inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual,
   return tc_tma_launches(m, n, k, dual) + (tc_presplit_wanted(m, n, k, dual, false) ? operands : 0);
 }
 
+// Returns true when the epilogue also wrote a0.Dlo (the lo image of D) for a
+// later product; operand lo images passed in a0 (Alo, Blo, ...) are used as
+// given and not recomputed.
 template <BenchId Bn, int V>
-inline void launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t s) {
+inline bool launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t s) {
   TcGemmArgs a = a0;
   a.tile_flags = ws.ensure_tile_flags();
   a.epoch = ++ws.tile_epoch;
+  bool dlo = false;
   if (tc_presplit_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0) && tma_ok(a.lda, a.ldb)) {
-    // distinct operand arrays and their storage extents (floats)
+    // distinct operand arrays without a given lo image, and their storage extents (floats)
     const float* ops[4] = {a.A, a.B, a.A2, a.B2};
-    const int64_t ext[4] = {
-        a.ta ? (int64_t)(a.K - 1) * a.lda + a.M : (int64_t)(a.M - 1) * a.lda + a.K,
-        a.tb ? (int64_t)(a.N - 1) * a.ldb + a.K : (int64_t)(a.K - 1) * a.ldb + a.N,
-        0, 0};
-    int64_t e[4] = {ext[0], ext[1], a.A2 ? ext[0] : 0, a.B2 ? ext[1] : 0};
+    const float* given[4] = {a.Alo, a.Blo, a.A2lo, a.B2lo};
+    const int64_t ext_a = a.ta ? (int64_t)(a.K - 1) * a.lda + a.M : (int64_t)(a.M - 1) * a.lda + a.K;
+    const int64_t ext_b = a.tb ? (int64_t)(a.N - 1) * a.ldb + a.K : (int64_t)(a.K - 1) * a.ldb + a.N;
+    const int64_t e[4] = {ext_a, ext_b, a.A2 ? ext_a : 0, a.B2 ? ext_b : 0};
     int64_t off[4], total = 0;
     for (int i = 0; i < 4; ++i) {
       off[i] = -1;
-      if (!ops[i]) continue;
+      if (!ops[i] || given[i]) continue;
       for (int j = 0; j < i; ++j)
-        if (ops[j] == ops[i] && e[j] == e[i]) off[i] = off[j];
+        if (!given[j] && ops[j] == ops[i] && e[j] == e[i]) off[i] = off[j];
       if (off[i] < 0) {
         off[i] = total;
         total += (e[i] + 63) / 64 * 64;  // 256-byte aligned images
       }
     }
-    float* lo = ws.ensure_scratch((size_t)total * sizeof(float));
-    if (lo) {
+    float* lo = total ? ws.ensure_scratch((size_t)total * sizeof(float)) : nullptr;
+    if (lo || !total) {
       bool done[4] = {false, false, false, false};
       for (int i = 0; i < 4; ++i) {
-        if (!ops[i] || done[i]) continue;
+        if (!ops[i] || given[i] || done[i]) continue;
         for (int j = i; j < 4; ++j)
-          if (ops[j] == ops[i] && off[j] == off[i]) done[j] = true;
+          if (!given[j] && ops[j] == ops[i] && off[j] == off[i]) done[j] = true;
         tc_split_lo<Bn, V><<<4 * 148, 256, 0, s>>>(ops[i], lo + off[i], e[i]);
       }
       TcGemmArgs b = a;
-      b.Alo = lo + off[0];
-      b.Blo = lo + off[1];
-      b.A2lo = a.A2 ? lo + off[2] : nullptr;
-      b.B2lo = a.B2 ? lo + off[3] : nullptr;
-      if (launch_tc_tma<Bn, V>(b, s)) return;
+      for (int i = 0; i < 4; ++i) {
+        const float* l = given[i] ? given[i] : (ops[i] ? lo + off[i] : nullptr);
+        (i == 0 ? b.Alo : i == 1 ? b.Blo : i == 2 ? b.A2lo : b.B2lo) = l;
+      }
+      if (launch_tc_tma<Bn, V>(b, s, &dlo)) return dlo;
     }
   }
-  if (!launch_tc_tma<Bn, V>(a, s)) launch_tc_gemm<Bn, V>(ws, a, s);
+  a.Alo = a.Blo = a.A2lo = a.B2lo = nullptr;  // converter warps split in-kernel
+  if (launch_tc_tma<Bn, V>(a, s, &dlo)) return dlo;
+  launch_tc_gemm<Bn, V>(ws, a, s);
+  return false;
 }
 
 }  // namespace pf
