@@ -149,10 +149,14 @@ def test_tensor_core_tiles_match_oracle(bench, gpu_backend):
 
 # Config-scale tensor-core paths the small sizes above never reach: CTA-pair
 # tiles without split-K (operands pre-split into lo images, TMA epilogue with
-# beta), pair tiles with a 2-way split (memset pre-pass + TMA add-reductions),
-# the K-concatenated SYR2K product, and CORR's upper-triangle split.
+# beta, chained lo images), pair tiles with a 2-way split (ordered in-kernel
+# hand-over, TMA add-reductions), the K-concatenated SYR2K product, and CORR's
+# upper-triangle split.
 TC_LARGE_SIZES = {
-    "2MM": [(2048, 2048, 256, 1024)],
+    # (2048, 2048, 256, 2048) / 3MM: the later product consumes the lo image
+    # that the earlier product's epilogue wrote
+    "2MM": [(2048, 2048, 256, 1024), (2048, 2048, 256, 2048)],
+    "3MM": [(2048, 2048, 256, 2048, 256)],
     "SYRK": [(2048, 512)],
     "SYR2K": [(2048, 256)],
     "CORR": [(2048, 256)],
