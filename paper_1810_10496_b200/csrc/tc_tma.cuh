@@ -1,28 +1,36 @@
-// Stage-2 contraction kernel, TMA generation: tcgen05 / TMEM 3xTF32 GEMM fed
+// Stage-2 contraction kernels, TMA generation: tcgen05 / TMEM 3xTF32 GEMM fed
 // directly from the raw fp32 operands.
 //
 //   D = alpha * op(A) op(B) + beta * Cin        (same contract as tc_gemm.cuh)
 //
-// Differences from the packed path (tc_gemm.cuh):
-//   * no pack kernel and no hi/lo copies in global memory: TMA tensor maps
-//     (cuTensorMapEncodeTiled, SWIZZLE_128B) load the raw fp32 tiles in either
-//     major-ness -- K-major tiles as one 128x32 box, MN-major tiles as four
-//     32x32 boxes -- straight into the canonical UMMA shared-memory layouts;
+// Operands:
+//   * TMA tensor maps (cuTensorMapEncodeTiled, SWIZZLE_128B) load the raw fp32
+//     tiles in either major-ness -- K-major tiles as one 128x32 box, MN-major
+//     tiles as four 32x32 boxes -- straight into the canonical UMMA
+//     shared-memory layouts;
 //   * the tensor core truncates fp32 to TF32 when it reads an operand, so the
-//     raw tile *is* the "hi" operand (hi = trunc_tf32(x)); four converter warps
-//     compute lo = x - trunc_tf32(x) elementwise into a second buffer (the
-//     operation is layout-agnostic, so one loop serves both major-nesses);
-//   * operand traffic per k block is halved (raw tiles only).
+//     raw tile *is* the "hi" operand (hi = trunc_tf32(x)); the "lo" operand
+//     x - trunc_tf32(x) is either TMA-loaded from a pre-split image in global
+//     memory (products without split-K: tc_split_lo, or the previous product's
+//     epilogue, or CORR's transpose pass) or computed by four converter warps
+//     into the stage's lo buffers (split-K products).
 // Precision: x = hi + lo exactly; the tensor core truncates lo to TF32
 // (|error| <= 2^-10 |lo| <= 2^-20 |x|); the dropped lo*lo term is ~2^-20.
 //
-// Warp roles (192 threads, 1 CTA/SM, 128x128 tile, 3-stage ring of
-// [A raw | B raw | A lo | B lo] = 64 KB):
+// Warp roles (192 threads, 1 CTA/SM, 3-stage ring of [A raw | B raw | A lo |
+// B lo] = 64 KB):
 //   warp 0 lane 0   TMA producer            full[s]  (expect_tx)
-//   warps 2..5      lo converters           ready[s] (one arrive per warp),
-//                   then the TMEM epilogue (warp w reads TMEM lanes 32*(w%4))
+//   warps 2..5      lo converters (or a pass-through arrive when pre-split)
+//                   -> ready[s]; then the epilogue (warp w reads TMEM lanes
+//                   32*(w%4)): TMA Cin loads, alpha/beta in place in shared
+//                   memory, TMA stores / add-reductions, optional lo image of D
 //   warp 1 lane 0   MMA issuer: 4 k-steps x {lo*hi, hi*lo, hi*hi}; commit -> empty[s]
-//   warp 1          TMEM allocation (128 columns)
+//   warp 1          TMEM allocation
+// tc_tma_kernel: one CTA per 128x128 tile (cta_group::1); tc_tma2_kernel: a
+// CTA pair per 256x256 tile (cta_group::2, each CTA streams half of B).
+// Split-K: beta pre-pass + TMA add-reductions (the GEMM launched as a
+// programmatic dependent launch) or, for beta = 0, an in-kernel ordered
+// hand-over through per-tile flags.
 #pragma once
 #include "pf_common.cuh"
 #include "tc_gemm.cuh"
