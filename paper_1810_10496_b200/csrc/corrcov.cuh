@@ -281,6 +281,10 @@ inline void run(Workspace& ws, cudaStream_t s) {
       // 16-byte pitches for the TMA maps (K tail beyond n reads as zero)
       const int np = (n + 3) / 4 * 4, mp = (m + 3) / 4 * 4;
       float* xt = ws.ensure_scratch((2 * (size_t)m * np + (size_t)m * mp) * sizeof(float));
+      if (!xt) {
+        launch_failed("CORR/COVAR stage 2: scratch allocation failed");
+        return;
+      }
       float* xt_lo = xt + (size_t)m * np;
       float* G = xt_lo + (size_t)m * np;
       reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt,

@@ -62,7 +62,7 @@ struct Run {
       // E's and F's lo images come out of their products' epilogues (when
       // those run pre-split), so G = E F needs no split pass of its own
       float* elo = ws.ensure_aux(((size_t)ni * nj + (size_t)nj * nl) * sizeof(float));
-      float* flo = elo + (size_t)ni * nj;
+      float* flo = elo ? elo + (size_t)ni * nj : nullptr;  // no aux buffer: both products split in-kernel
       TcGemmArgs p1{ni, nj, nk, 1.f, 0.f, A, nk, false, B, nj, false, nullptr, nullptr, nullptr, nj, E, nj, 0};
       p1.Dlo = elo;
       const bool have_elo = launch_contraction<B_3MM, V>(ws, p1, s);

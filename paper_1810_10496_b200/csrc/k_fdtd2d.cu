@@ -291,6 +291,10 @@ void tb_sequence(Workspace& ws, cudaStream_t s) {
   const int nx = (int)ws.dims.d[0], ny = (int)ws.dims.d[1], tmax = (int)ws.dims.d[2];
   const size_t n = (size_t)nx * ny;
   float* scratch = ws.ensure_scratch(3 * n * sizeof(float));
+  if (!scratch) {
+    launch_failed("FDTD-2D: double-buffer allocation failed");
+    return;
+  }
   float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
   static bool configured = false;
   if (!configured) {
@@ -328,6 +332,10 @@ void fused_sequence(Workspace& ws, cudaStream_t s) {
   const int nx = (int)ws.dims.d[0], ny = (int)ws.dims.d[1], tmax = (int)ws.dims.d[2];
   const size_t n = (size_t)nx * ny;
   float* scratch = ws.ensure_scratch(3 * n * sizeof(float));
+  if (!scratch) {
+    launch_failed("FDTD-2D: double-buffer allocation failed");
+    return;
+  }
   float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
   const bool vec = ny % 4 == 0;
   dim3 block(kBX, kBY), grid(cdiv(ny, kBX), cdiv(nx, kBY));

@@ -279,6 +279,10 @@ template <BenchId Bn, int V>
 void launch_panel(Workspace& ws, cudaStream_t s) {
   const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
   float* scratch = ws.ensure_scratch((size_t)n * m * sizeof(float) + (size_t)n * sizeof(int));
+  if (!scratch) {
+    launch_failed("GRAMSCHM panel: scratch allocation failed");
+    return;
+  }
   float* qbuf = scratch;
   int* flags = reinterpret_cast<int*>(scratch + (size_t)n * m);
   cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), s);
@@ -660,6 +664,10 @@ template <BenchId Bn, int V>
 void launch_panel2(Workspace& ws, cudaStream_t s) {
   const int m = (int)ws.dims.d[0], n = (int)ws.dims.d[1];
   float* scratch = ws.ensure_scratch((size_t)n * kP2Rows * sizeof(float) + 2 * (size_t)n * sizeof(int));
+  if (!scratch) {
+    launch_failed("GRAMSCHM panel2: scratch allocation failed");
+    return;
+  }
   float* qbuf = scratch;
   int* flags = reinterpret_cast<int*>(scratch + (size_t)n * kP2Rows);  // [n] panel flags, [n] column flags
   cudaMemsetAsync(flags, 0, 2 * (size_t)n * sizeof(int), s);

@@ -456,7 +456,10 @@ inline void launch_tc_gemm(Workspace& ws, const TcGemmArgs& a, cudaStream_t s) {
   const int kblocks = kp / kTcBK;
   const size_t asz = (size_t)mp * kp, bsz = (size_t)np * kp;
   float* scr = ws.ensure_scratch((2 * asz + 2 * bsz) * sizeof(float));
-  if (!scr) return;  // allocation failure surfaces as a missing launch -> output mismatch
+  if (!scr) {
+    launch_failed("tcgen05 packed path: operand scratch allocation failed");
+    return;
+  }
   float* ahi = scr;
   float* alo = ahi + asz;
   float* bhi = alo + asz;
