@@ -49,8 +49,10 @@ struct Run {
       launch_simt_gemm<B_SYRK, V, false, true, false>(
           SimtGemmArgs{n, n, m, kAlpha, kBeta, A, m, A, m, nullptr, nullptr, C, n, C, n, 0}, s);
     } else {
-      launch_contraction<B_SYRK, V>(
-          ws, TcGemmArgs{n, n, m, kAlpha, kBeta, A, m, false, A, m, true, nullptr, nullptr, C, n, C, n, 0}, s);
+      // op(A) op(B) is symmetric: upper tiles only, mirrored below the diagonal
+      TcGemmArgs g{n, n, m, kAlpha, kBeta, A, m, false, A, m, true, nullptr, nullptr, C, n, C, n, 0};
+      g.sym = 1;
+      launch_contraction<B_SYRK, V>(ws, g, s);
     }
   }
 };
@@ -59,7 +61,9 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 
 int64_t elems(int a, const Dims& d) { return a == 0 ? d.d[0] * d.d[1] : d.d[0] * d.d[0]; }
 int64_t launches(int v, const Dims& d) {
-  return kTab.v[v].stage == 2 ? tc_launches(d.d[0], d.d[0], d.d[1], tma_ok(d.d[1], d.d[1]), false, 1) : 1;
+  if (kTab.v[v].stage != 2) return 1;
+  // symmetric TMA path: lo split pass + beta pre-pass + GEMM
+  return tma_ok(d.d[1], d.d[1]) ? 3 : tc_launches(d.d[0], d.d[0], d.d[1], false, false, 1);
 }
 double alg_bytes(const Dims& d) { return 4.0 * ((double)d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }
 double alg_flops(const Dims& d) { return 2.0 * (double)d.d[0] * d.d[0] * d.d[1]; }

@@ -58,6 +58,10 @@ struct TcGemmArgs {
   // optional: the epilogue also writes lo = D - trunc_tf32(D) here (pitch ldd)
   // for a later product that consumes D as an operand
   float* Dlo = nullptr;
+  // symmetric product (M == N, op(A) op(B) symmetric: SYRK, SYR2K): only tiles
+  // on or above the diagonal are computed; off-diagonal tiles are also
+  // added, transposed, below the diagonal (beta pre-pass + add-reductions)
+  int sym = 0;
 };
 
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;
@@ -435,6 +439,28 @@ __global__ void __launch_bounds__(256) tc_prescale(float* D, int ldd, const floa
   const int m = blockIdx.y;
   if (n >= N) return;
   D[(size_t)m * ldd + n] = beta != 0.f ? beta * Cin[(size_t)m * ldc + n] : 0.f;
+}
+
+// Contiguous form (ldd == ldc == N, 16-byte aligned): float4, four loads in
+// flight per thread, grid-stride.
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) tc_prescale_flat(float4* __restrict__ D, const float4* __restrict__ Cin,
+                                                        int64_t n4, float beta) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = Cin[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      D[i + u * stride] = make_float4(beta * v[u].x, beta * v[u].y, beta * v[u].z, beta * v[u].w);
+  }
+  for (; i < n4; i += stride) {
+    const float4 v = Cin[i];
+    D[i] = make_float4(beta * v.x, beta * v.y, beta * v.z, beta * v.w);
+  }
 }
 
 template <BenchId Bn, int V, int BN>

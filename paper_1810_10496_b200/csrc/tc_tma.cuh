@@ -57,6 +57,7 @@ struct TmaParams {
   int tma_epi;
   CUtensorMap tdl;               // lo image of D (valid iff dlo)
   int dlo;
+  int sym;                       // mirror off-diagonal tiles (add-reductions)
   int* tile_flags;               // ordered split-K: split 0 stores, the others add after its flag
   int epoch;
   int creduce;                   // split-K partials reduced across the z-cluster through DSMEM (tc_tma_kernel)
@@ -149,13 +150,15 @@ __device__ __forceinline__ void reduce_add_2d(const CUtensorMap* map, uint32_t s
 // 1024-byte aligned, ncols / 32 * 4 KB; bar: this warp's mbarrier (phase 0).
 __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr, int ncols, int row0, int col0,
                                              bool split, uint8_t* buf, uint32_t bar, int lane,
-                                             bool writes_done = false, uint8_t* lobuf = nullptr) {
+                                             bool writes_done = false, uint8_t* lobuf = nullptr,
+                                             bool mirror = false) {
   if (row0 >= p.M) return;  // warp-uniform
   const int nch = min(ncols / 32, (p.N - col0 + 31) / 32);
   const bool use_c = !split && p.beta != 0.f;
   const bool want_lo = p.dlo && !split && lobuf != nullptr;  // 4 x 4 KB ring of lo chunks
+  const bool want_mirror = mirror && split && lobuf != nullptr;  // same ring: transposed chunks
   const uint32_t sbuf = tc::smem_u32(buf);
-  const uint32_t slo = want_lo ? tc::smem_u32(lobuf) : 0u;
+  const uint32_t slo = (want_lo || want_mirror) ? tc::smem_u32(lobuf) : 0u;
   if (use_c && lane == 0) {
     tc::mbar_expect_tx(bar, (uint32_t)nch * 4096u);
     for (int c = 0; c < nch; ++c) load_2d(sbuf + c * 4096, &p.tc, col0 + c * 32, row0, bar);
@@ -177,11 +180,20 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr,
                         fmaf(p.beta, ci.w, v.w));
       }
       *slot = v;
-      if (want_lo) {
-        if (j == 0 && c >= 4) {  // lo slot c % 4 is free once chunk c - 4's stores have read it
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
-          __syncwarp();
+      if ((want_lo || want_mirror) && j == 0 && c >= 4) {  // ring slot c % 4 is free once chunk c - 4's
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");  // stores have read it
+        __syncwarp();
+      }
+      if (want_mirror) {  // transposed box: row = this column, column = lane (conflict-free 4-byte stores)
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int jr = 4 * j + e;
+          *reinterpret_cast<float*>(lobuf + (c & 3) * 4096 + jr * 128 + (((lane >> 2) ^ (jr & 7)) << 4) +
+                                    ((lane & 3) << 2)) = vv[e];
         }
+      }
+      if (want_lo) {
         float4* lslot = reinterpret_cast<float4*>(lobuf + (c & 3) * 4096 + lane * 128) + (j ^ (lane & 7));
         *lslot = make_float4(v.x - trunc_tf32(v.x), v.y - trunc_tf32(v.y), v.z - trunc_tf32(v.z),
                              v.w - trunc_tf32(v.w));
@@ -195,6 +207,7 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr,
       else
         store_2d(&p.td, sbuf + c * 4096, col0 + c * 32, row0);
       if (want_lo) store_2d(&p.tdl, slo + (c & 3) * 4096, col0 + c * 32, row0);
+      if (want_mirror) reduce_add_2d(&p.td, slo + (c & 3) * 4096, row0, col0 + c * 32);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
@@ -345,7 +358,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
   const int m0 = mb * 128, n0 = nb * 128;
   const int kb0 = blockIdx.z * p.kb_per_split;
   const int nkb = min(p.kblocks - kb0, p.kb_per_split);
-  const bool split = gridDim.z > 1 && !p.creduce;
+  const bool split = (gridDim.z > 1 && !p.creduce) || p.sym;  // sym: beta pre-pass + add-reductions
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
@@ -450,7 +463,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
       tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
-                        tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384);
+                        tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
+                        p.sym && nb != mb);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
@@ -565,7 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
   const int n0 = nb * 256;                    // accumulator columns (both CTAs)
   const int kb0 = blockIdx.z * p.kb_per_split;
   const int nkb = min(p.kblocks - kb0, p.kb_per_split);
-  const bool split = gridDim.z > 1;
+  const bool split = gridDim.z > 1 || p.sym;  // sym: beta pre-pass + add-reductions
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
@@ -666,7 +680,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
       tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
-                        tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384);
+                        tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
+                        p.sym && nb != mb);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
@@ -848,15 +863,18 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   const int kblocks = a.A2 ? 2 * kb1 : kb1;
   // split-K problems: beta pre-pass + TMA add-reductions (PF_TC_CREDUCE=1:
   // reduce the partials inside a z-cluster of single-CTA tiles instead)
-  const int cz = tc_cluster_splits(a.M, a.N, kblocks);
+  // symmetric products compute the upper tiles and mirror the rest (needs the
+  // TMA epilogue; otherwise the full product is computed)
+  p.sym = (a.sym && p.tma_epi && a.M == a.N) ? 1 : 0;
+  const int cz = p.sym ? 1 : tc_cluster_splits(a.M, a.N, kblocks);
   p.creduce = cz > 1 ? 1 : 0;
   // CTA pairs only for problems that fill the GPU without split-K (GEMM 512^3:
   // 128 single-CTA split-K tiles beat 64 split-K pair halves)
-  const bool up = a.upper_only != 0;
+  const bool up = a.upper_only != 0 || p.sym;
   const bool pair = !p.creduce && tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
   const int zs = p.creduce ? cz : tc_tma_splits(a.M, a.N, kblocks, pair, up);
   const int per = (kblocks + zs - 1) / zs;
-  p.dlo = (a.Dlo && p.tma_epi && zs == 1 && !p.creduce && reinterpret_cast<uintptr_t>(a.Dlo) % 16 == 0 &&
+  p.dlo = (a.Dlo && p.tma_epi && zs == 1 && !p.creduce && !p.sym && reinterpret_cast<uintptr_t>(a.Dlo) % 16 == 0 &&
            tma::make_map(&p.tdl, a.Dlo, a.N, a.M, a.ldd, 32, 32, false))
               ? 1
               : 0;
@@ -865,13 +883,19 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   // ordered hand-over only where the alternative pre-pass is a memset (beta
   // == 0): with beta != 0 split 0's Cin load + store serialise the splits
   // (GEMM 512^3: 17.4 us vs 15.3 us with the beta pre-pass)
-  const bool ordered =
-      zs > 1 && !p.creduce && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlags && a.beta == 0.f;
+  const bool ordered = zs > 1 && !p.creduce && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlags &&
+                       a.beta == 0.f;
+  const bool prepass = (zs > 1 || p.sym) && !p.creduce && !ordered;  // beta * Cin (or zero) before the adds
   p.tile_flags = ordered ? a.tile_flags : nullptr;
   p.epoch = a.epoch;
-  if (zs > 1 && !p.creduce && !ordered) {
+  if (prepass) {
     if (a.beta == 0.f)
       cudaMemset2DAsync(a.D, (size_t)a.ldd * sizeof(float), 0, (size_t)a.N * sizeof(float), a.M, s);
+    else if (a.ldd == a.N && a.ldc == a.N && a.N % 4 == 0 && reinterpret_cast<uintptr_t>(a.D) % 16 == 0 &&
+             reinterpret_cast<uintptr_t>(a.Cin) % 16 == 0)
+      tc_prescale_flat<Bn, V><<<4 * 148, 256, 0, s>>>(reinterpret_cast<float4*>(a.D),
+                                                       reinterpret_cast<const float4*>(a.Cin),
+                                                       (int64_t)a.M * a.N / 4, a.beta);
     else
       tc_prescale<Bn, V><<<dim3(cdiv(a.N, 256), a.M), 256, 0, s>>>(a.D, a.ldd, a.Cin, a.ldc, a.M, a.N, a.beta);
   }
@@ -886,7 +910,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   p.ldc = a.ldc;
   p.D = a.D;
   p.ldd = a.ldd;
-  p.upper_only = a.upper_only;
+  p.upper_only = a.upper_only || p.sym;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tc_tma_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
@@ -912,7 +936,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
     // after a beta pre-pass the GEMM is a programmatic dependent launch: its
     // prologue and mainloop overlap the pre-pass (griddepcontrol.wait gates
     // only the epilogue's add-reductions)
-    const bool pdl = zs > 1 && !ordered;
+    const bool pdl = prepass;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = pair ? dim3(2 * cdiv(a.N, 256), cdiv(a.M, 256), zs) : dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs);
     cfg.blockDim = dim3(kTmaThreads);
@@ -1013,7 +1037,9 @@ inline bool launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t
   a.tile_flags = ws.ensure_tile_flags();
   a.epoch = ++ws.tile_epoch;
   bool dlo = false;
-  if (tc_presplit_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0) && tma_ok(a.lda, a.ldb)) {
+  // symmetric products split-K their upper tiles but still profit from the
+  // pre-split operands (SYRK: one lo pass serves both operands)
+  if ((a.sym || tc_presplit_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0)) && tma_ok(a.lda, a.ldb)) {
     // distinct operand arrays without a given lo image, and their storage extents (floats)
     const float* ops[4] = {a.A, a.B, a.A2, a.B2};
     const float* given[4] = {a.Alo, a.Blo, a.A2lo, a.B2lo};

@@ -50,6 +50,8 @@ def main() -> int:
         elif bound.startswith("tensor"):
             tf = r["best_tflops"]
             ach, frac = f"{tf:.1f} TF/s", f"{tf / tc:.0%} of 3xTF32 ({tf / MMA_ONLY_TFLOPS:.0%} of MMA-only)"
+            if b in ("SYRK", "SYR2K"):  # symmetric: half of the standard flops are computed
+                frac += "; standard flops, half computed (symmetry)"
         elif bound == "l2":
             ach, frac = f"{r['best_gbs']:.0f} GB/s (L2-resident)", "—"
         else:
