@@ -5,10 +5,10 @@
 // row, ex update, hz update), i.e. 3*TMAX launches.  Phase ordering had no
 // effect on the paper's GPU.  Stage 1: one fused kernel per
 // step on double-buffered fields (each thread recomputes the two neighbour
-// updates hz needs), TMAX launches; stage 2: temporal blocking (4 time steps
-// per launch on 64x64 shared-memory regions with a 4-cell halo), the launch
-// sequence captured once as a CUDA graph.  At 2048^2 the six 16 MiB fields
-// stay L2-resident.
+// updates hz needs), TMAX launches; stage 2: temporal blocking in registers
+// (6 time steps per launch on 64 x 128 regions held in registers, 6-cell
+// halo), the launch sequence captured once as a CUDA graph.  At 2048^2 the
+// six 16 MiB fields stay L2-resident.
 #include "pf_common.cuh"
 
 #include <algorithm>
@@ -313,17 +313,135 @@ void tb_sequence(Workspace& ws, cudaStream_t s) {
     for (int f = 0; f < 3; ++f) cudaMemcpyAsync(buf[0][f], buf[1][f], n * sizeof(float), cudaMemcpyDeviceToDevice, s);
 }
 
-// Stage-2 time steps per launch: 4 by default on 64x64 regions (2048^2 x 500:
-// 5.77 ms vs 6.16 ms for the per-step fused sequence); PF_FDTD_TB=0 selects the
-// per-step sequence, PF_FDTD_TB=8 a deeper blocking (6.47 ms; A/B runs).  128x128
-// regions (one 512-thread CTA per SM) measured 6.5-7.7 ms for 4-16 steps.
+// ---- stage 2, register-tiled temporal blocking.  A 128-thread CTA holds a
+// 32-row x 128-column region of the three fields in REGISTERS: warp w owns
+// rows 8w .. 8w+7, lane l columns 4l .. 4l+3 (one float4 per row and field).
+// Neighbours along j come from the adjacent lane (shuffles), along i from the
+// thread's own registers, and across warps from one shared row per warp and
+// field (hz's last row before the ey/ex phase, ey's first row before the hz
+// phase): two block barriers per time step and no per-cell shared-memory
+// traffic.  kRT steps per launch; halo kRT rows and one float4 of columns, so
+// the CTA writes rows kRT .. 31-kRT and columns 4 .. 123.
+template <BenchId Bn, int V, int kRT, int kW>
+__global__ void __launch_bounds__(32 * kW) step_rt(const float* __restrict__ fict, const float* __restrict__ ex0,
+                                               const float* __restrict__ ey0, const float* __restrict__ hz0,
+                                               float* __restrict__ ex1, float* __restrict__ ey1,
+                                               float* __restrict__ hz1, int nx, int ny, int t0, int steps) {
+  constexpr int kR = 8, kRows = kR * kW, kOutRows = kRows - 2 * kRT;
+  __shared__ float4 hz_last[kW][32], ey_first[kW][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gi0 = blockIdx.y * kOutRows - kRT + warp * kR;  // global row of this thread's r = 0
+  const int gj = blockIdx.x * 120 - 4 + 4 * lane;          // global column of this thread's c = 0
+  const bool col_in = gj >= 0 && gj < ny;                    // ny % 4 == 0: a float4 is all in or all out
+  float ex[kR][4], ey[kR][4], hz[kR][4];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int gi = gi0 + r;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a;
+    if (col_in && gi >= 0 && gi < nx) {
+      const size_t o = (size_t)gi * ny + gj;
+      a = __ldcg(reinterpret_cast<const float4*>(ex0 + o));
+      b = __ldcg(reinterpret_cast<const float4*>(ey0 + o));
+      c = __ldcg(reinterpret_cast<const float4*>(hz0 + o));
+    }
+    ex[r][0] = a.x, ex[r][1] = a.y, ex[r][2] = a.z, ex[r][3] = a.w;
+    ey[r][0] = b.x, ey[r][1] = b.y, ey[r][2] = b.z, ey[r][3] = b.w;
+    hz[r][0] = c.x, hz[r][1] = c.y, hz[r][2] = c.z, hz[r][3] = c.w;
+  }
+  for (int st = 0; st < steps; ++st) {
+    const float src = __ldg(fict + t0 + st);
+    // hz row above this warp's first row (region edge for warp 0: garbage allowed)
+    hz_last[warp][lane] = make_float4(hz[kR - 1][0], hz[kR - 1][1], hz[kR - 1][2], hz[kR - 1][3]);
+    __syncthreads();
+    const float4 hu = warp > 0 ? hz_last[warp - 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // ey / ex phase
+#pragma unroll
+    for (int r = kR - 1; r >= 0; --r) {  // bottom-up: hz is not modified here, order is free
+      const int gi = gi0 + r;
+      const float up[4] = {r > 0 ? hz[r - 1][0] : hu.x, r > 0 ? hz[r - 1][1] : hu.y, r > 0 ? hz[r - 1][2] : hu.z,
+                           r > 0 ? hz[r - 1][3] : hu.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ey[r][c] = gi == 0 ? src : upd_e(ey[r][c], hz[r][c], up[c]);
+      const float hl = __shfl_up_sync(0xffffffffu, hz[r][3], 1);  // lane 0: region edge
+      ex[r][0] = gj == 0 ? ex[r][0] : upd_e(ex[r][0], hz[r][0], hl);
+#pragma unroll
+      for (int c = 1; c < 4; ++c) ex[r][c] = upd_e(ex[r][c], hz[r][c], hz[r][c - 1]);
+    }
+    // ey row below this warp's last row (region edge for warp 3)
+    ey_first[warp][lane] = make_float4(ey[0][0], ey[0][1], ey[0][2], ey[0][3]);
+    __syncthreads();
+    const float4 ed = warp < kW - 1 ? ey_first[warp + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // hz phase
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int gi = gi0 + r;
+      const float down[4] = {r < kR - 1 ? ey[r + 1][0] : ed.x, r < kR - 1 ? ey[r + 1][1] : ed.y,
+                             r < kR - 1 ? ey[r + 1][2] : ed.z, r < kR - 1 ? ey[r + 1][3] : ed.w};
+      const float xr = __shfl_down_sync(0xffffffffu, ex[r][0], 1);  // lane 31: region edge
+      if (gi < nx - 1) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float xn = c < 3 ? ex[r][c + 1] : xr;
+          if (gj + c < ny - 1) hz[r][c] = upd_h(hz[r][c], xn, ex[r][c], down[c], ey[r][c]);
+        }
+      }
+    }
+  }
+  // ---- store rows kRT .. 31-kRT of the region, lanes 1 .. 30
+  if (lane == 0 || lane == 31 || !col_in) return;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int lr = warp * kR + r, gi = gi0 + r;
+    if (lr < kRT || lr >= kRows - kRT || gi < 0 || gi >= nx) continue;
+    const size_t o = (size_t)gi * ny + gj;
+    __stcg(reinterpret_cast<float4*>(ex1 + o), make_float4(ex[r][0], ex[r][1], ex[r][2], ex[r][3]));
+    __stcg(reinterpret_cast<float4*>(ey1 + o), make_float4(ey[r][0], ey[r][1], ey[r][2], ey[r][3]));
+    __stcg(reinterpret_cast<float4*>(hz1 + o), make_float4(hz[r][0], hz[r][1], hz[r][2], hz[r][3]));
+  }
+}
+
+template <BenchId Bn, int V, int kRT, int kW>
+void rt_sequence(Workspace& ws, cudaStream_t s) {
+  const int nx = (int)ws.dims.d[0], ny = (int)ws.dims.d[1], tmax = (int)ws.dims.d[2];
+  const size_t n = (size_t)nx * ny;
+  float* scratch = ws.ensure_scratch(3 * n * sizeof(float));
+  if (!scratch) {
+    launch_failed("FDTD-2D: double-buffer allocation failed");
+    return;
+  }
+  float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
+  const dim3 grid(cdiv(ny, 120), cdiv(nx, 8 * kW - 2 * kRT));
+  int launches = 0;
+  for (int t = 0; t < tmax; t += kRT, ++launches) {
+    float** src = buf[launches & 1];
+    float** dst = buf[(launches + 1) & 1];
+    step_rt<Bn, V, kRT, kW><<<grid, 32 * kW, 0, s>>>(ws.a.p[0], src[0], src[1], src[2], dst[0], dst[1], dst[2], nx, ny, t,
+                                            std::min(kRT, tmax - t));
+  }
+  if (launches & 1)
+    for (int f = 0; f < 3; ++f) cudaMemcpyAsync(buf[0][f], buf[1][f], n * sizeof(float), cudaMemcpyDeviceToDevice, s);
+}
+
+// Stage 2 = the register-tiled temporal blocking (kRTSteps time steps per
+// launch on 64-row x 128-column register regions, 8 warps): 2.09 ms for
+// 2048^2 x 500 steps vs 5.77 ms for the shared-memory blocking (64x64
+// regions, 4 steps; PF_FDTD_TB=4) and 6.16 ms for the per-step fused sequence
+// (PF_FDTD_TB=0).  Register-tiled shapes measured and dropped: 4 warps x 4-6
+// steps (2.37-2.62 ms), 8 warps x 5/7/8 steps (2.15-2.33 ms), 16 warps x
+// 8/10/12 steps (2.04-2.45 ms; 12 steps ties at one 512-thread CTA per SM).
+constexpr int kRTSteps = 6, kRTWarps = 8;
 inline int fdtd_tb_depth() {
   static const int d = [] {
     const char* e = std::getenv("PF_FDTD_TB");
-    const int v = e ? std::atoi(e) : 4;
-    return (v == 0 || v == 8) ? v : 4;  // depths keep region origins float4-aligned
+    const int v = e ? std::atoi(e) : -1;
+    return (v == 0 || v == 4) ? v : -1;
   }();
   return d;
+}
+// time steps per stage-2 launch
+inline int fdtd_steps_per_launch() {
+  const int d = fdtd_tb_depth();
+  return d == 0 ? 1 : d == 4 ? 4 : kRTSteps;
 }
 inline bool fdtd_tb_disabled() { return fdtd_tb_depth() == 0; }
 
@@ -376,8 +494,8 @@ struct Run {
       const bool tb = ny % 4 == 0 && !fdtd_tb_disabled();
       const int d = fdtd_tb_depth();
       cudaGraphExec_t g = !tb      ? cached_graph(ws, V + 1000, &fused_sequence<B_FDTD2D, V>)
-                          : d == 8 ? cached_graph(ws, V + 3000, &tb_sequence<B_FDTD2D, V, 8, 64, 256>)
-                                   : cached_graph(ws, V, &tb_sequence<B_FDTD2D, V, 4, 64, 256>);
+                          : d == 4 ? cached_graph(ws, V + 2000, &tb_sequence<B_FDTD2D, V, 4, 64, 256>)
+                                   : cached_graph(ws, V, &rt_sequence<B_FDTD2D, V, kRTSteps, kRTWarps>);
       cudaGraphLaunch(g, s);
     }
   }
@@ -388,7 +506,10 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 int64_t elems(int a, const Dims& d) { return a == 0 ? d.d[2] : d.d[0] * d.d[1]; }
 int64_t launches(int v, const Dims& d) {
   const int st = kTab.v[v].stage;
-  if (st == 2 && d.d[1] % 4 == 0 && !fdtd_tb_disabled()) return (d.d[2] + fdtd_tb_depth() - 1) / fdtd_tb_depth();
+  if (st == 2 && d.d[1] % 4 == 0 && !fdtd_tb_disabled()) {
+    const int steps = fdtd_steps_per_launch();
+    return (d.d[2] + steps - 1) / steps;
+  }
   return st == 0 ? 3 * d.d[2] : d.d[2];
 }
 // fused compulsory traffic per step: read ex, ey, hz, write ex, ey, hz
