@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --steps 2 --warmup 3 --e2e-steps 0 --cpu-evals 0 --num-sequences 200 > gpurun_out/bench_under_ncu.log 2>&1
 for spec in "ATAX 16384,16384 stage=2 s2_fused" "GESUMMV 16384 stage=2 gesummv_s2" \
             "2MM 2048,2048,2048,2048 stage=2 tc_tma2_kernel" "3DCONV 256,256,256 stage=2 conv3d_s2d" \
-            "2DCONV 4096,4096 stage=2 conv2d_s2" "FDTD-2D 2048,2048,20 stage=2 step_tb" "GEMM 512,512,512 stage=2 tc_tma_kernel" \
+            "2DCONV 4096,4096 stage=2 conv2d_s2" "FDTD-2D 2048,2048,24 stage=2 step_rt" "GEMM 512,512,512 stage=2 tc_tma_kernel" \
             "SYRK 2048,2048 stage=2 tc_tma2_kernel" "CORR 2048,2048 stage=2 tc_tma2_kernel"; do
   set -- $spec
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$4 -s 1 -c 1 \
