@@ -60,7 +60,6 @@ struct TmaParams {
   int sym;                       // mirror off-diagonal tiles (add-reductions)
   int* tile_flags;               // ordered split-K: split 0 stores, the others add after its flag
   int epoch;
-  int creduce;                   // split-K partials reduced across the z-cluster through DSMEM (tc_tma_kernel)
   int kblocks, kb_per_split, kb1;
   int a_mn, b_mn;                // operand is MN-major (contiguous along M / N)
   int M, N;
@@ -267,83 +266,6 @@ __device__ __forceinline__ void load_operands(const TmaParams& p, bool second, b
   }
 }
 
-// ---- split-K reduction across a z-cluster (GEMM-sized problems: one launch,
-// no beta pre-pass, no atomics).  Partials are staged row-major 128 x 128
-// fp32 (512-byte rows) with the 16-byte chunk index XORed by row % 8, so the
-// lane-per-row TMEM stores and the row-contiguous reads are conflict-free.
-__device__ __forceinline__ uint32_t partial_off(int row, int chunk) {
-  return (uint32_t)row * 512u + (uint32_t)((chunk ^ (row & 7)) * 16);
-}
-
-__device__ __forceinline__ void stage_partial(uint32_t taddr, uint8_t* buf, int row) {
-  const uint32_t sbuf = tc::smem_u32(buf);
-#pragma unroll 1
-  for (int c = 0; c < 4; ++c) {
-    uint32_t r[32];
-    tc::tmem_ld32(taddr + (uint32_t)(c * 32), r);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      sts128(sbuf + partial_off(row, c * 8 + j),
-             make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                         __uint_as_float(r[4 * j + 3])));
-  }
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ float4 ld_dsmem128(uint32_t cluster_addr) {
-  float4 v;
-  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-      : "r"(cluster_addr)
-      : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void reduce_partials(const TmaParams& p, uint8_t* buf, int m0, int n0, int S, int rank) {
-  const uint32_t sbuf = tc::smem_u32(buf);
-  const int r0 = 128 * rank / S, r1 = 128 * (rank + 1) / S;
-  const int items = (r1 - r0) * 32;  // float4 chunks of this CTA's rows
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int row = r0 + it / 32, chunk = it % 32;
-    const int grow = m0 + row, gcol = n0 + 4 * chunk;
-    if (grow >= p.M || gcol >= p.N) continue;
-    const uint32_t off = partial_off(row, chunk);
-    // all S remote loads in flight before the (fixed-order, reproducible) sum
-    float4 part[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (q < S) {
-        uint32_t peer;
-        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(sbuf + off), "r"(q));
-        part[q] = ld_dsmem128(peer);
-      }
-    }
-    float4 acc = part[0];
-#pragma unroll
-    for (int q = 1; q < 8; ++q) {
-      if (q < S) {
-        acc.x += part[q].x;
-        acc.y += part[q].y;
-        acc.z += part[q].z;
-        acc.w += part[q].w;
-      }
-    }
-    float o[4] = {p.alpha * acc.x, p.alpha * acc.y, p.alpha * acc.z, p.alpha * acc.w};
-    const float* crow = p.Cin + (size_t)grow * p.ldc;
-    float* drow = p.D + (size_t)grow * p.ldd;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (gcol + e < p.N) {
-        if (p.beta != 0.f) o[e] = fmaf(p.beta, crow[gcol + e], o[e]);
-        drow[gcol + e] = o[e];
-      }
-    }
-  }
-}
-
 }  // namespace tma
 
 template <BenchId Bn, int V>
@@ -358,7 +280,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
   const int m0 = mb * 128, n0 = nb * 128;
   const int kb0 = blockIdx.z * p.kb_per_split;
   const int nkb = min(p.kblocks - kb0, p.kb_per_split);
-  const bool split = (gridDim.z > 1 && !p.creduce) || p.sym;  // sym: beta pre-pass + add-reductions
+  const bool split = gridDim.z > 1 || p.sym;  // sym: beta pre-pass + add-reductions
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
@@ -455,9 +377,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
     tc::mbar_wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
     const int quad = warp & 3;
-    if (p.creduce)
-      tma::stage_partial(tmem + ((uint32_t)(quad * 32) << 16), smem, quad * 32 + lane);
-    else if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
+    if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
@@ -473,13 +393,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
     else if (!(p.diag & 8))
       tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                           p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
-  }
-  if (p.creduce) {
-    // every CTA of the z-cluster holds a 128x128 partial in its ring; CTA r
-    // sums rows [r*128/S, (r+1)*128/S) over all S partials (DSMEM reads)
-    tma::cluster_sync_all();
-    tma::reduce_partials(p, smem, m0, n0, (int)gridDim.z, (int)blockIdx.z);
-    tma::cluster_sync_all();  // peers stop reading this CTA's ring
   }
   tc::fence_before();
   __syncthreads();
@@ -798,23 +711,6 @@ inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair, bool uppe
   return (kblocks + per - 1) / per;
 }
 
-// z-cluster size for split-K with an in-cluster reduction: 128x128 tiles,
-// up to 8 (portable cluster limit) k-splits of >= 1 k block when the output
-// alone would leave more than half the SMs idle; 1 = no cluster split.
-inline int tc_cluster_splits(int64_t m, int64_t n, int kblocks) {
-  static const bool enabled = [] {  // opt-in (PF_TC_CREDUCE=1): slower than the TMA add-reduction on B200
-    const char* e = std::getenv("PF_TC_CREDUCE");
-    return e && e[0] == '1';
-  }();
-  if (!enabled) return 1;
-  const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
-  if (tiles >= 74 || kblocks < 2) return 1;
-  int z = (int)std::min<int64_t>(8, std::max<int64_t>(1, 148 / tiles));
-  z = std::min(z, kblocks);
-  const int per = (kblocks + z - 1) / z;
-  return (kblocks + per - 1) / per;
-}
-
 template <BenchId Bn, int V>
 inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written = nullptr) {
   if (dlo_written) *dlo_written = false;
@@ -861,20 +757,20 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
                     : 0;
   const int kb1 = (a.K + 31) / 32;
   const int kblocks = a.A2 ? 2 * kb1 : kb1;
-  // split-K problems: beta pre-pass + TMA add-reductions (PF_TC_CREDUCE=1:
-  // reduce the partials inside a z-cluster of single-CTA tiles instead)
+  // split-K problems: beta pre-pass + TMA add-reductions, or the ordered
+  // hand-over for beta = 0.  (Reducing the partials inside a z-cluster through
+  // DSMEM was measured slower on B200 -- 24.5 vs 15.3 us for GEMM 512^3 -- and
+  // removed.)
   // symmetric products compute the upper tiles and mirror the rest (needs the
   // TMA epilogue; otherwise the full product is computed)
   p.sym = (a.sym && p.tma_epi && a.M == a.N) ? 1 : 0;
-  const int cz = p.sym ? 1 : tc_cluster_splits(a.M, a.N, kblocks);
-  p.creduce = cz > 1 ? 1 : 0;
   // CTA pairs only for problems that fill the GPU without split-K (GEMM 512^3:
   // 128 single-CTA split-K tiles beat 64 split-K pair halves)
   const bool up = a.upper_only != 0 || p.sym;
-  const bool pair = !p.creduce && tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
-  const int zs = p.creduce ? cz : tc_tma_splits(a.M, a.N, kblocks, pair, up);
+  const bool pair = tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
+  const int zs = tc_tma_splits(a.M, a.N, kblocks, pair, up);
   const int per = (kblocks + zs - 1) / zs;
-  p.dlo = (a.Dlo && p.tma_epi && zs == 1 && !p.creduce && !p.sym && reinterpret_cast<uintptr_t>(a.Dlo) % 16 == 0 &&
+  p.dlo = (a.Dlo && p.tma_epi && zs == 1 && !p.sym && reinterpret_cast<uintptr_t>(a.Dlo) % 16 == 0 &&
            tma::make_map(&p.tdl, a.Dlo, a.N, a.M, a.ldd, 32, 32, false))
               ? 1
               : 0;
@@ -883,9 +779,9 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   // ordered hand-over only where the alternative pre-pass is a memset (beta
   // == 0): with beta != 0 split 0's Cin load + store serialise the splits
   // (GEMM 512^3: 17.4 us vs 15.3 us with the beta pre-pass)
-  const bool ordered = zs > 1 && !p.creduce && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlags &&
+  const bool ordered = zs > 1 && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlags &&
                        a.beta == 0.f;
-  const bool prepass = (zs > 1 || p.sym) && !p.creduce && !ordered;  // beta * Cin (or zero) before the adds
+  const bool prepass = (zs > 1 || p.sym) && !ordered;  // beta * Cin (or zero) before the adds
   p.tile_flags = ordered ? a.tile_flags : nullptr;
   p.epoch = a.epoch;
   if (prepass) {
@@ -917,22 +813,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
     cudaFuncSetAttribute(tc_tma2_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     configured = true;
   }
-  if (p.creduce) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cdiv(a.N, 128), cdiv(a.M, 128), zs);
-    cfg.blockDim = dim3(kTmaThreads);
-    cfg.dynamicSmemBytes = kTmaSmem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = (unsigned)zs;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, tc_tma_kernel<Bn, V>, p) != cudaSuccess)
-      launch_failed("tcgen05 split-K cluster launch rejected");
-  } else {
+  {
     // after a beta pre-pass the GEMM is a programmatic dependent launch: its
     // prologue and mainloop overlap the pre-pass (griddepcontrol.wait gates
     // only the epilogue's add-reductions)
@@ -958,7 +839,6 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
 inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false, bool upper = false,
                                bool beta_zero = false) {
   const int kblocks = (int)((dual ? 2 : 1) * ((k + 31) / 32));
-  if (tc_cluster_splits(m, n, kblocks) > 1) return 1;
   const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, upper) <= 2;
   const bool split = tc_tma_splits(m, n, kblocks, pair, upper) > 1;
   return split && !beta_zero ? 2 : 1;  // beta pre-pass, or the in-kernel ordered hand-over
