@@ -221,12 +221,10 @@ __global__ void __launch_bounds__(kS2Threads) conv3d_s2(const __grid_constant__ 
           // (j-1, k-1) (j-1, k+1) (j, k+1) (j+1, k+1) and (j-1, k) (j, k) (j+1, k)
           const float xmm = v[r][e], xmp = v[r][e + 2], xzp = v[r + 1][e + 2], xpp = v[r + 2][e + 2];
           const float xmz = v[r][e + 1], xzz = v[r + 1][e + 1], xpz = v[r + 2][e + 1];
-          const float P = c13 * xmm + c23 * xmm + c33 * xmm + c13 * xmp + c23 * xzp + c33 * xpp;
-          const float Z = c12 * xmz + c22 * xzz + c32 * xpz;
-          const float M = c11 * xmm + c21 * xmm + c31 * xmm + c11 * xmp + c21 * xzp + c31 * xpp;
-          out[e] = mz[r][e] + P;  // outputs of plane q-1 (valid for q > i_begin)
-          mz[r][e] = mn[r][e] + Z;
-          mn[r][e] = M;
+          // folded repeated taps, 11 FMAs per output (as in the direct form)
+          out[e] = fmaf(c33, xpp, fmaf(c23, xzp, fmaf(c13, xmp, fmaf(c13 + c23 + c33, xmm, mz[r][e]))));
+          mz[r][e] = fmaf(c32, xpz, fmaf(c22, xzz, fmaf(c12, xmz, mn[r][e])));
+          mn[r][e] = fmaf(c31, xpp, fmaf(c21, xzp, fmaf(c11, xmp, (c11 + c21 + c31) * xmm)));
         }
         const int i = q - 1, j = jr + r;
         if (q > i_begin && j <= p.nj - 2 && kq < p.nk) {
