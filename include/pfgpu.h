@@ -127,7 +127,10 @@ int pf_run_e2e(pf_ws* ws, int variant, int samples, float* const* host_in, float
  *   [restore in-place state] [L2 flush] start_i -> variant run -> end_i
  *   [D2H of every output array into non-NULL host_out[a]]
  * ms_each[i] = end_i - start_i (the variant's device time); *ms_total =
- * first recorded event to last (the whole batch, copies included). */
+ * first recorded event to last (the whole batch, copies included).  The
+ * upload of a workspace's first evaluation in the batch is issued up front on
+ * a per-device copy stream (it overlaps earlier candidates; the evaluation
+ * waits for it); later uploads into an already used workspace stay in order. */
 typedef struct pf_eval {
   pf_ws* ws;
   int variant;

@@ -65,6 +65,7 @@ struct FlushBuf {
 };
 std::mutex g_flush_mu;
 FlushBuf g_flush[64];
+cudaStream_t g_copy_stream[64];  // per-device upload stream of pf_eval_batch (guarded by g_flush_mu)
 
 int flush_l2(int device, cudaStream_t s) {
   FlushBuf* fb;
@@ -254,6 +255,7 @@ int pf_device_reset(int device) {
   {
     std::lock_guard<std::mutex> lk(g_flush_mu);
     g_flush[device] = FlushBuf{};  // memory dies with the context
+    g_copy_stream[device] = nullptr;  // so does the upload stream
   }
   int rc = set_device(device);
   if (rc) return rc;
@@ -558,17 +560,53 @@ int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush, float* ms
   for (int i = 0; i < n; ++i) PF_CUDA(cudaStreamSynchronize(evals[i].ws->stream));
   cudaStream_t st = evals[0].ws->stream;
   thread_local std::vector<cudaEvent_t> pool;
-  while ((int)pool.size() < 2 * n + 2) {
+  while ((int)pool.size() < 3 * n + 2) {
     cudaEvent_t e;
-    PF_CUDA(cudaEventCreate(&e));
+    PF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
     pool.push_back(e);
   }
   cudaEvent_t first = pool[2 * n], last = pool[2 * n + 1];
   PF_CUDA(cudaEventRecord(first, st));
+  // Input uploads of a workspace's FIRST evaluation in the batch go to a copy
+  // stream, all of them up front, so the copy engine streams the next
+  // workspace's inputs while the current one's candidates run; each such
+  // evaluation waits only for its own upload (and the pristine snapshot).
+  // Repeated uploads into a workspace already in use stay on the compute
+  // stream, in order.
+  cudaStream_t cs = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_flush_mu);
+    if (!g_copy_stream[device]) PF_CUDA(cudaStreamCreateWithFlags(&g_copy_stream[device], cudaStreamNonBlocking));
+    cs = g_copy_stream[device];
+  }
+  PF_CUDA(cudaStreamWaitEvent(cs, first, 0));  // uploads start inside the timed region
+  std::vector<char> prefetched(n, 0);
+  {
+    std::vector<const pf_ws*> seen;
+    for (int i = 0; i < n; ++i) {
+      pf_ws* ws = evals[i].ws;
+      bool first_use = true;
+      for (const pf_ws* w : seen) first_use &= (w != ws);
+      if (first_use) seen.push_back(ws);
+      if (!first_use || !evals[i].host_in) continue;
+      const BenchDesc* d = ws->desc;
+      for (int a = 0; a < d->narrays; ++a) {
+        if (!evals[i].host_in[a] || d->arrays[a].role == OUT) continue;
+        const size_t bytes = ws->elems[a] * sizeof(float);
+        PF_CUDA(cudaMemcpyAsync(ws->a.p[a], evals[i].host_in[a], bytes, cudaMemcpyHostToDevice, cs));
+        if (ws->pristine[a])
+          PF_CUDA(cudaMemcpyAsync(ws->pristine[a], ws->a.p[a], bytes, cudaMemcpyDeviceToDevice, cs));
+      }
+      PF_CUDA(cudaEventRecord(pool[2 * n + 2 + i], cs));
+      prefetched[i] = 1;
+    }
+  }
   for (int i = 0; i < n; ++i) {
     pf_ws* ws = evals[i].ws;
     const BenchDesc* d = ws->desc;
-    if (evals[i].host_in) {
+    if (prefetched[i]) {
+      PF_CUDA(cudaStreamWaitEvent(st, pool[2 * n + 2 + i], 0));
+    } else if (evals[i].host_in) {
       for (int a = 0; a < d->narrays; ++a) {
         if (!evals[i].host_in[a] || d->arrays[a].role == OUT) continue;
         const size_t bytes = ws->elems[a] * sizeof(float);
