@@ -1,29 +1,38 @@
 #!/usr/bin/env python3
-"""Benchmark: candidate-evaluation throughput on the memory-bound BLAS-2 set.
+"""Benchmark: candidate evaluations/s of the exploration loop on the BLAS-2 set.
 
 Workload (BASELINE.json configs[1]): ATAX, BICG, MVT and GESUMMV at
-N = 16384, fp32.  One *step* is one exploration round of the hot path: every
-fresh candidate that ``explore`` would evaluate on a 1000-order seeded stream
-(the distinct artifacts, plus the baseline) gets one device-timed
-measurement run through the C-ABI (``pf_eval_batch``).  ``value`` is the
-whole-job evaluations/s (sum over ranks / max step time over ranks).
+N = 16384, fp32.  One *step* is one exploration round of the product path
+-- ``explore()`` (explorer.py, the reference's loop restated) on each of the
+four kernels over a fresh 1000-order stream (max_len 256, the default pass
+catalog), through ``B200Backend`` with its device work batched ahead
+(``sweep.explore_suite``: compile lookup, digest dedup / REUSED records,
+validation run + output compare, one CUDA-event-timed measurement run per
+fresh candidate after an L2 flush).  ``value`` is fresh evaluations/s (the
+paper's unit: one validation + one measurement of a new artifact), whole
+job (sum over ranks / max step time over ranks); every step draws new
+orders (seed changes per step and rank), so compiles and candidates are new
+work each step.
 
 Each rank drives one GPU (one process per GPU, torchrun) with its own
-candidate stream (seed 1729 + 7919*rank): weak scaling, no data-path
-collective; torch.distributed is used only for the barrier and
-the max-over-ranks timing reduction.
+order streams: weak scaling, no data-path collective;
+torch.distributed is used only for the barrier and the max-over-ranks
+timing reduction.
 
-Extra keys: ``roofline`` (dominant specialized kernel, HBM bytes vs the
-measured peak), ``e2e`` (same metric with the inputs uploaded from pinned
-host memory and outputs read back inside the timed region),
-``cpu_baseline`` (the C oracle on the host cores, bounded sample),
-``geomean_speedup`` (best candidate vs baseline variant per kernel),
-``clocks`` (nvidia-smi sampled during the timed region), ``gpu_launches``.
+Extra keys: ``e2e`` (the same explore() round with every input array --
+validation and measurement, 5.4 GB per step -- uploaded from pinned host
+memory inside the timed region, outputs read back), ``roofline`` (GESUMMV's
+stage-2 kernel as timed inside the steps vs the measured HBM peak),
+``cpu_baseline`` (the reference's own path on the host: its unmodified
+explore() + ToolchainBackend with the oracle runner, a bounded sample; plus
+the oracle kernels single-thread / all threads and the reference explore()
+on its simulator), ``geomean_speedup``, ``clocks``, ``gpu_launches``.
 
-``--impl reference`` times the reference-side CPU implementation of the same
-workload (the oracle port: PolyBench/GPU is not in /root/reference, and the
-reference package itself is pure Python with no kernel code) on all host
-threads and prints its own line.
+``--impl reference`` runs the reference's path alone on the host (rank 0):
+its unmodified explore() driving ToolchainBackend, whose runner process
+computes each kernel with the CPU oracle on all host threads (oracle/
+pf_cpu_runner; PolyBench/GPU is not part of the reference), over a bounded
+sample of orders per kernel and step.
 """
 
 from __future__ import annotations
@@ -37,6 +46,7 @@ import subprocess
 import sys
 import threading
 import time
+from dataclasses import replace
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -56,6 +66,10 @@ def _peaks() -> dict:
 
 def _dims(bench: str, n: int) -> tuple[int, ...]:
     return (n, n) if bench in ("ATAX", "BICG") else (n,)
+
+
+def _workload(n: int) -> str:
+    return f"BLAS-2 set ATAX/BICG/MVT/GESUMMV, N={n} fp32 (BASELINE configs[1]): explore() rounds"
 
 
 # ---------------------------------------------------------------- clocks
@@ -112,61 +126,103 @@ class ClockSampler:
 from paper_1810_10496_b200.dist import Dist  # noqa: E402
 
 
-# ---------------------------------------------------------------- CPU side
-def cpu_eval_rate(n: int, evals_target: int, threads: int = 0) -> dict:
-    """The C oracle on the host: evaluations/s over the 4 kernels at size n."""
-    from oracle import oracle as orc
+class StepTimer:
+    """Device-side timing of one step: CUDA events on torch's current stream,
+    recorded after a full device synchronize on both sides (the step is a
+    host + device pipeline: the events bracket all of it)."""
 
-    used = orc.set_threads(threads)
-    arrays = {b: orc.generate(b, _dims(b, n)) for b in KERNELS}
-    done, secs = 0, 0.0
-    while done < evals_target:
-        for b in KERNELS:
-            work = [a.copy() if i in (1, 2) and b == "MVT" else a for i, a in enumerate(arrays[b])]
-            t0 = time.perf_counter()
-            orc.run(b, _dims(b, n), work)
-            secs += time.perf_counter() - t0
-            done += 1
-    return {"value": done / secs, "unit": "evals/s", "cores": used, "kind": "port", "seconds": secs, "evals": done,
-            "sample": f"{done} oracle evaluations ({'/'.join(KERNELS)} round-robin) at N={n}, fp64 accumulation, "
-                      f"{used} pthreads"}
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.pairs = []
+
+    def __enter__(self):
+        t = self.torch
+        t.cuda.synchronize()
+        self.a, self.b = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        self.a.record()
+        return self
+
+    def __exit__(self, *exc):
+        self.b.record()
+        self.torch.cuda.synchronize()
+        self.pairs.append(self.a.elapsed_time(self.b))
+
+    @property
+    def ms(self) -> float:
+        return self.pairs[-1]
+
+
+# ---------------------------------------------------------------- reference-side CPU legs
+def _ref_setup(n: int):
+    from oracle import ref_arm
+    from paper_1810_10496_b200 import passmodel
+
+    pf = ref_arm.reference_engine()
+    if pf is None:
+        return None
+    work = ref_arm.workdir()
+    be = ref_arm.toolchain_backend(pf, work)
+    dims = {b: _dims(b, n) for b in KERNELS}
+    cases = ref_arm.kernel_cases(pf, KERNELS, dims, work)
+    names = [p.name for p in passmodel.default_catalog().passes]
+    return ref_arm, pf, be, cases, names, dims
+
+
+def cpu_baseline(n: int, orders: int) -> dict:
+    """The reference's CPU path on a bounded sample (rank 0, N=1)."""
+    setup = _ref_setup(n)
+    from oracle import ref_arm
+
+    dims = {b: _dims(b, n) for b in KERNELS}
+    out = {"cpu_model": ref_arm.cpu_model(), "host_cores": ref_arm.cores()}
+    out.update(ref_arm.oracle_rates(KERNELS, dims, min_seconds=2.0))
+    if setup is None:
+        mt = out["oracle_mt"]
+        out.update({"value": mt["evals_per_s"], "unit": "evals/s", "cores": mt["cores"], "kind": "port",
+                    "sample": f"{mt['evals']} oracle kernel evaluations at N={n} (reference package absent)"})
+        return out
+    ref_arm_mod, pf, be, cases, names, _ = setup
+    fresh, recs, secs = ref_arm.explore_step(pf, be, cases, names, orders, 1729)
+    out.update({"value": fresh / secs, "unit": "evals/s", "cores": ref_arm.cores(), "kind": "port",
+                "sample": f"phaseforge.explore + ToolchainBackend (oracle runner, all threads), {orders} orders x "
+                          f"{len(KERNELS)} kernels at N={n}: {fresh} fresh evaluations in {secs:.2f} s"})
+    out["reference_simulator_explore"] = ref_arm.simulator_rate(pf, names)
+    return out
 
 
 def run_reference(args, dist: Dist) -> int:
     if dist.rank != 0:
         return 0
-    from oracle import oracle as orc
-
-    threads = orc.set_threads(0)
-    n = args.n
-    arrays = {b: orc.generate(b, _dims(b, n)) for b in KERNELS}
-
-    def step() -> tuple[int, float]:
-        t = 0.0
-        for b in KERNELS:
-            work = [a.copy() if b == "MVT" and i in (1, 2) else a for i, a in enumerate(arrays[b])]
-            t0 = time.perf_counter()
-            orc.run(b, _dims(b, n), work)
-            t += time.perf_counter() - t0
-        return len(KERNELS), t
-
-    for _ in range(args.warmup):
-        step()
-    evals, secs = 0, 0.0
-    for _ in range(args.steps):
-        e, t = step()
-        evals += e
-        secs += t
-    value = evals / secs
+    setup = _ref_setup(args.n)
+    if setup is None:
+        print(json.dumps({"impl": "reference", "unavailable": "reference package not importable "
+                          "(neither /root/reference/pkg/src nor baseline/_ref)"}), flush=True)
+        return 0
+    ref_arm, pf, be, cases, names, _ = setup
+    for w in range(args.warmup):
+        ref_arm.explore_step(pf, be, cases, names, args.ref_orders, 1729 + 104729 * (w + 1))
+    fresh = recs = valid = 0
+    secs = 0.0
+    for s in range(args.steps):
+        f, r, t = ref_arm.explore_step(pf, be, cases, names, args.ref_orders, 1729 + 104729 * (1000 + s))
+        fresh, recs, secs, valid = fresh + f, recs + r, secs + t, valid + ref_arm.explore_step.valid
+    value = fresh / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (PolyBench/GPU init formulas)",
-        "config": {"workload": "BLAS-2 set ATAX/BICG/MVT/GESUMMV, N=%d fp32 (BASELINE configs[1])" % n,
-                   "n": n, "kernels": list(KERNELS)},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} steps x {len(KERNELS)} oracle evaluations at N={n}"},
+        "config": {"workload": _workload(args.n), "n": args.n, "kernels": list(KERNELS),
+                   "orders_per_kernel_per_step": args.ref_orders, "max_len": 256,
+                   "path": "phaseforge.explore (unmodified) -> ToolchainBackend: 4 compile-stage processes per "
+                           "candidate, 1 runner process per execute (oracle/pf_cpu_runner, CPU oracle kernels)"},
+        "fresh_evaluations": fresh, "records": recs, "valid_fraction": valid / max(1, fresh),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": ref_arm.cores(), "kind": "port",
+                         "cpu_model": ref_arm.cpu_model(),
+                         "sample": f"{args.steps} steps x {len(KERNELS)} kernels x {args.ref_orders} orders "
+                                   f"(every order a distinct artifact) at N={args.n}"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -174,141 +230,177 @@ def run_reference(args, dist: Dist) -> int:
 
 
 # ---------------------------------------------------------------- GPU side
-def run_gpu(args, dist: Dist) -> int:
+def _stock_host_inputs(be, cases, keep):
+    """Pinned host copies of every generated input array (validation and
+    measurement workspaces) -- the data the runner would load -- and the
+    bytes per upload round."""
+    from paper_1810_10496_b200 import _abi, registry
+    from paper_1810_10496_b200.backend.b200 import _Staging
+    import ctypes
     import numpy as np
 
-    from paper_1810_10496_b200 import _abi
+    table, h2d = {}, 0
+    for case in cases:
+        for kind, desc in (("validation", case.validation_input), ("measurement", case.measurement_input)):
+            bench, dims = registry.parse_descriptor(desc)
+            ws = be.workspace(bench, dims, True, -1)
+            ptrs = {}
+            for a, (_, role, _) in enumerate(ws.arrays):
+                if role == _abi.ROLE_OUT:
+                    continue
+                st = _Staging(_abi.lib(), 4 * ws.elems[a])
+                keep.append(st)
+                np.ctypeslib.as_array((ctypes.c_float * ws.elems[a]).from_address(st.ptr))[:] = ws.download(a)
+                ptrs[a] = st.ptr
+                h2d += 4 * ws.elems[a]
+            table[(case.id, kind)] = ptrs
+    return table, h2d
+
+
+def run_gpu(args, dist: Dist) -> int:
+    from paper_1810_10496_b200 import passmodel, registry
     from paper_1810_10496_b200.backend.b200 import B200Backend, alg_work, family
-    from paper_1810_10496_b200.sweep import candidate_set, evaluate_round, launches_of
+    from paper_1810_10496_b200.campaign import kernel_config
+    from paper_1810_10496_b200.explorer import ExplorationConfig, RecordStatus
+    from paper_1810_10496_b200.sweep import explore_suite
 
     peaks = _peaks()
     device = dist.local
-    be = B200Backend(device=device, samples=1)
+    be = B200Backend(device=device, samples=1, flush_l2=True)
     n = args.n
-    seed = 1729 + 7919 * dist.rank
-    items = []           # (ws, variant) in evaluation order
-    per_kernel = {}
-    for k, b in enumerate(KERNELS):
-        ws = be.workspace(b, _dims(b, n), True, -1)
-        cands = candidate_set(be, b, num_sequences=args.num_sequences, max_len=256, seed=seed + k)
-        per_kernel[b] = {"ws": ws, "cands": cands}
-        items += [(ws, c.variant) for c in cands]
+    cases = registry.build_suite(be, size="config", benches=KERNELS) if n == 16384 else [
+        registry.kernel_case(b, measurement_dims=_dims(b, n)) for b in KERNELS]
+    if n != 16384:
+        cases = [replace(c, reference_outputs=be.baseline_outputs(c)) for c in cases]
+    catalog = passmodel.default_catalog()
+    base = ExplorationConfig(num_sequences=args.num_sequences, max_len=256)
 
-    for _ in range(max(3, args.warmup)):
-        evaluate_round(items, flush_l2=True)
+    def configs(step: int):
+        return [replace(kernel_config(base, c), seed=1729 + 7919 * dist.rank + 104729 * step + k)
+                for k, c in enumerate(cases)]
+
+    stage2 = {b: next(v for v in range(len(family(b).knobs)) if family(b).knobs[v][0] == 2) for b in KERNELS}
+    s2_digest = {b: be.artifact(b, v).digest for b, v in stage2.items()}
+
+    def fresh_of(recs):
+        return [r for r in recs if r.status not in (RecordStatus.REUSED, RecordStatus.NO_IR)]
+
+    def one_step(step, timer, host_inputs=None):
+        runs0, launches0 = be.device_runs, be.kernel_launches
+        with timer:
+            out = explore_suite(cases, catalog, configs(step), be, host_inputs)
+        fresh = {k: fresh_of(v) for k, v in out.items()}
+        return out, fresh, be.device_runs - runs0, be.kernel_launches - launches0
+
+    timer = StepTimer()
+    for w in range(max(3, args.warmup)):
+        one_step(-1 - w, timer)
 
     dist.barrier()
-    t_steps = []
-    ms_acc = [0.0] * len(items)
+    n_fresh = n_records = n_runs = n_launch = 0
+    s2_ms = {b: [] for b in KERNELS}
+    valid = 0
+    best = {}  # kernel -> (fastest valid record time ms, order)
+    batch0 = be.batch_ms
     with ClockSampler(device) as clocks:
-        for _ in range(args.steps):
-            ms_each, ms_total = evaluate_round(items, flush_l2=True)
-            t_steps.append(ms_total)
-            for i, m in enumerate(ms_each):
-                ms_acc[i] += m
+        for s in range(args.steps):
+            recs, fresh, runs, launches = one_step(s, timer)
+            n_fresh += sum(len(v) for v in fresh.values())
+            n_records += sum(len(v) for v in recs.values())
+            valid += sum(1 for v in fresh.values() for r in v if r.status is RecordStatus.VALID)
+            n_runs += runs
+            n_launch += launches
+            for b in KERNELS:
+                s2_ms[b] += [1e3 * r.wall_time for r in fresh[b] if r.artifact_digest == s2_digest[b]
+                             and r.wall_time]
+                top = recs[b][0]  # explore's output is sorted: fastest valid record first
+                if top.status is RecordStatus.VALID and (b not in best or 1e3 * top.wall_time < best[b][0]):
+                    best[b] = (1e3 * top.wall_time, top.order)
     dist.barrier()
-    local_s = sum(t_steps) / 1e3
+    step_ms = timer.pairs[-args.steps:]
+    local_s = sum(step_ms) / 1e3
     max_s = dist.max(local_s)
-    total_evals = dist.sum(len(items) * args.steps)
-    value = total_evals / max_s
+    value = dist.sum(n_fresh) / max_s
+    batch_busy = (be.batch_ms - batch0) / 1e3 / local_s
 
-    # ---- per-kernel analysis (device event times of this rank)
-    mean_ms = [m / args.steps for m in ms_acc]
+    # ---- end to end: inputs uploaded from pinned host memory every step
+    e2e = None
+    if args.e2e_steps > 0:
+        keep = []
+        host_inputs, h2d = _stock_host_inputs(be, cases, keep)
+        one_step(-100, StepTimer(), host_inputs)  # warm
+        et = StepTimer()
+        e_fresh, d2h = 0, 0
+        dist.barrier()
+        for s in range(args.e2e_steps):
+            recs, fresh, _, _ = one_step(10000 + s, et, host_inputs)
+            e_fresh += sum(len(v) for v in fresh.values())
+            d2h += sum(4 * len(c.reference_outputs) * len(fresh[c.id]) for c in cases)
+        dist.barrier()
+        e_max = dist.max(sum(et.pairs) / 1e3)
+        e2e = {"value": dist.sum(e_fresh) / e_max, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h // args.e2e_steps, "steps": args.e2e_steps,
+               "path": "sweep.explore_suite -> explore() x4 with B200Backend.prefetch_many(host_inputs=pinned "
+                       "copies of every input array); validation outputs read back per candidate"}
+        be._drain()
+        for st in keep:
+            st.free()
+
+    # ---- per-kernel report (outside the timed region)
     report = {}
-    best_stage2 = None
-    for b in KERNELS:
-        ws = per_kernel[b]["ws"]
-        idx = [i for i, (w, _) in enumerate(items) if w is ws]
-        fam = family(b)
-        base_i = idx[0]
-        best_i = min(idx, key=lambda i: mean_ms[i])
-        bytes_, _ = alg_work(b, ws.dims)
-        report[b] = {
-            "candidates": len(idx),
-            "baseline_ms": mean_ms[base_i],
-            "best_ms": mean_ms[best_i],
-            "best_variant": fam.key(items[best_i][1]),
-            "speedup": mean_ms[base_i] / mean_ms[best_i],
-            "best_gbs": bytes_ / (mean_ms[best_i] * 1e-3) / 1e9,
-            "time_share": sum(mean_ms[i] for i in idx) / sum(mean_ms),
-        }
-        for i in idx:
-            if fam.knobs[items[i][1]][0] == 2:
-                tot = mean_ms[i]
-                if best_stage2 is None or tot > best_stage2[1]:
-                    best_stage2 = (b, tot, i)
+    for c in cases:
+        b = c.id
+        _, dims = registry.parse_descriptor(c.measurement_input)
+        t_base = be.time_variant(b, dims, 0, samples=3) * 1e3  # the empty order (nvcc-shaped baseline)
+        t_best, order = best[b]
+        bytes_, _ = alg_work(b, dims)
+        report[b] = {"baseline_ms": t_base, "best_ms": t_best,
+                     "best_variant": family(b).key(be.variant_for(c, order)[1]),
+                     "speedup": t_base / t_best, "best_gbs": bytes_ / (t_best * 1e-3) / 1e9,
+                     "stage2_ms_in_steps": statistics.mean(s2_ms[b]) if s2_ms[b] else None}
     geo = math.exp(sum(math.log(r["speedup"]) for r in report.values()) / len(report))
 
     roofline = None
-    if best_stage2:
-        b, ms, i = best_stage2
-        ws = items[i][0]
-        bytes_, _ = alg_work(b, ws.dims)
+    rb = "GESUMMV"
+    if s2_ms[rb]:
+        ms = statistics.mean(s2_ms[rb])
+        bytes_, _ = alg_work(rb, _dims(rb, n))
         achieved = bytes_ / (ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": args.traffic or ncu_traffic(b, items[i][1]),
-                    "kernel": f"{b} {family(b).key(items[i][1])}",
-                    "alg_bytes_per_launch": bytes_, "mean_launch_ms": ms,
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": args.traffic or ncu_traffic(rb, stage2[rb]),
+                    "kernel": f"{rb} {family(rb).key(stage2[rb])}", "alg_bytes_per_launch": bytes_,
+                    "mean_launch_ms": ms, "launches_timed": len(s2_ms[rb]),
                     "peak_source": peaks["source"] + " (burst copy, MEASURED_PEAKS.json)"}
 
-    # ---- end to end: inputs from pinned host memory, outputs read back
-    e2e = None
-    if args.e2e_steps > 0:
-        lib = _abi.lib()
-        host_in, host_out, pinned = {}, {}, []
-        h2d = d2h = 0
-        for b in KERNELS:
-            ws = per_kernel[b]["ws"]
-            hin, hout = {}, {}
-            for a, (_, role, is_out) in enumerate(ws.arrays):
-                nbytes = ws.elems[a] * 4
-                if role != _abi.ROLE_OUT:
-                    p = ctypes_alloc(lib, nbytes, pinned)
-                    src = ws.download(a)
-                    ctypes_copy(p, src)
-                    hin[a] = p
-                    h2d += nbytes
-                if is_out:
-                    hout[a] = ctypes_alloc(lib, nbytes, pinned)
-                    d2h += nbytes * len(per_kernel[b]["cands"])
-            host_in[ws], host_out[ws] = hin, hout
-        evaluate_round(items, flush_l2=True, host_in=host_in, host_out=host_out)  # warm
-        dist.barrier()
-        e2e_ms = []
-        for _ in range(args.e2e_steps):
-            _, tot = evaluate_round(items, flush_l2=True, host_in=host_in, host_out=host_out)
-            e2e_ms.append(tot)
-        dist.barrier()
-        e2e_max = dist.max(sum(e2e_ms) / 1e3)
-        e2e_val = dist.sum(len(items) * args.e2e_steps) / e2e_max
-        e2e = {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "steps": args.e2e_steps, "path": "pf_eval_batch with pinned host_in/host_out (C-ABI)"}
-        for p in pinned:
-            lib.pf_host_free(p)
-
     cpu = None
-    if dist.rank == 0 and dist.world == 1 and args.cpu_evals > 0:
-        cpu = cpu_eval_rate(n, args.cpu_evals)
+    if dist.rank == 0 and dist.world == 1 and args.cpu_orders > 0:
+        cpu = cpu_baseline(n, args.cpu_orders)
 
-    launches = launches_of(items) * args.steps
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": dist.world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": 1e3 * max_s / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (PolyBench/GPU init formulas generated on device)",
-            "config": {"workload": f"BLAS-2 set ATAX/BICG/MVT/GESUMMV, N={n} fp32 (BASELINE configs[1])",
-                       "n": n, "kernels": list(KERNELS), "orders_per_kernel": args.num_sequences,
-                       "evals_per_step_per_gpu": len(items),
-                       "l2": "inputs larger than L2 (A is 1-2 GiB per kernel) and L2 flushed (2x L2 memset) "
-                             "before every candidate",
-                       "parallelism": f"candidate sharding x{dist.world} (independent streams)"},
+            "config": {"workload": _workload(n), "n": n, "kernels": list(KERNELS),
+                       "orders_per_kernel": args.num_sequences, "max_len": 256,
+                       "catalog": "20 Table-1 passes + 4 staging passes (passmodel.DEFAULT_CATALOG_PASSES)",
+                       "measurement": "B200Backend(samples=1): one CUDA-event-timed run per fresh candidate "
+                                      "(first use of a variant: 2 warm-up runs), L2 flushed before it",
+                       "l2": "inputs larger than L2 (A is 1-2 GiB per kernel) and L2 flushed (2x L2 memset + "
+                             "read) before every timed run",
+                       "parallelism": f"candidate streams x{dist.world} (one process per GPU, independent)"},
+            "fresh_evaluations_per_step": n_fresh / args.steps,
+            "candidate_records_per_s": dist.sum(n_records) / max_s,
+            "device_runs_per_s": dist.sum(n_runs) / max_s,
+            "valid_fraction": valid / max(1, n_fresh),
+            "device_busy_fraction": batch_busy,
             "geomean_speedup": geo,
             "per_kernel": report,
             "roofline": roofline,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": launches,
+            "gpu_launches": n_launch,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -329,23 +421,6 @@ def ncu_traffic(bench: str, variant: int):
     return entry["traffic"] if entry else None
 
 
-def ctypes_alloc(lib, nbytes: int, keep: list):
-    import ctypes
-
-    p = ctypes.c_void_p()
-    from paper_1810_10496_b200 import _abi
-
-    _abi.check(lib.pf_host_alloc(nbytes, ctypes.byref(p)))
-    keep.append(p)
-    return p.value
-
-
-def ctypes_copy(ptr: int, src) -> None:
-    import ctypes
-
-    ctypes.memmove(ptr, src.ctypes.data, src.nbytes)
-
-
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -355,7 +430,8 @@ def main() -> int:
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--num-sequences", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-evals", type=int, default=8)
+    ap.add_argument("--cpu-orders", type=int, default=2, help="orders per kernel in the cpu_baseline sample")
+    ap.add_argument("--ref-orders", type=int, default=2, help="orders per kernel per step of --impl reference")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the roofline kernel from an ncu --set full capture")
     args = ap.parse_args()

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PFGPU_ABI_VERSION 1
+#define PFGPU_ABI_VERSION 2
 
 /* error codes */
 #define PF_OK 0
@@ -100,6 +100,13 @@ int pf_ws_generate(pf_ws* ws, int stock, uint64_t seed, int64_t instance);
  * whose inputs live in (pinned) host memory. */
 int pf_ws_upload(pf_ws* ws, int array, const float* host, int64_t n);
 int pf_ws_download(pf_ws* ws, int array, float* host, int64_t n);
+/* Asynchronous upload (host should be pinned: pf_host_alloc): enqueued on the
+ * device's copy stream after the work already enqueued on the workspace, and
+ * every later use of the workspace (any pf_* call, pf_eval_batch included)
+ * is ordered after it.  Returns without waiting, so the copy engine streams
+ * one workspace's inputs while another workspace's candidates run (the
+ * runner's input load of toolchain.py:216-273, overlapped). */
+int pf_ws_upload_async(pf_ws* ws, int array, const float* host, int64_t n);
 /* Restore INOUT arrays and zero OUT arrays (enqueued, not timed). */
 int pf_ws_restore(pf_ws* ws);
 /* Device pointer of an array (for zero-copy interop; never freed by caller). */
@@ -124,9 +131,9 @@ int pf_run_e2e(pf_ws* ws, int variant, int samples, float* const* host_in, float
  * enqueued back to back on one stream (all workspaces on one device) with no
  * host synchronisation between candidates.  For evaluation i:
  *   [H2D of every non-NULL host_in[a] into ws (the runner's input upload)]
- *   [restore in-place state] [L2 flush] start_i -> variant run -> end_i
+ *   [restore in-place state] [L2 flush] start_i -> `batch` x variant run -> end_i
  *   [D2H of every output array into non-NULL host_out[a]]
- * ms_each[i] = end_i - start_i (the variant's device time); *ms_total =
+ * ms_each[i] = (end_i - start_i) / batch (one run's device time); *ms_total =
  * first recorded event to last (the whole batch, copies included).  The
  * upload of a workspace's first evaluation in the batch is issued up front on
  * a per-device copy stream (it overlaps earlier candidates; the evaluation
@@ -136,6 +143,8 @@ typedef struct pf_eval {
   int variant;
   float* const* host_in;  /* NULL or array-indexed host pointers */
   float* const* host_out; /* NULL or array-indexed host pointers */
+  int batch;              /* runs between the events; 0 or 1 = one run (us-scale kernels use more) */
+  int no_flush;           /* 1: no L2 flush before this evaluation (untimed validation runs) */
 } pf_eval;
 int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush_l2, float* ms_each, float* ms_total);
 

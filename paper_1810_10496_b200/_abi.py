@@ -66,6 +66,7 @@ def _declare(lib) -> None:
         "pf_ws_generate": (c_int, [c_void_p, c_int, c_uint64, c_int64]),
         "pf_ws_upload": (c_int, [c_void_p, c_int, c_void_p, c_int64]),
         "pf_ws_download": (c_int, [c_void_p, c_int, c_void_p, c_int64]),
+        "pf_ws_upload_async": (c_int, [c_void_p, c_int, c_void_p, c_int64]),
         "pf_ws_restore": (c_int, [c_void_p]),
         "pf_ws_array_ptr": (c_int, [c_void_p, c_int, POINTER(c_void_p)]),
         "pf_run": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, POINTER(c_float)]),
@@ -107,7 +108,8 @@ def check(rc: int) -> None:
 class PfEval(ctypes.Structure):
     """Mirror of ``struct pf_eval`` (include/pfgpu.h)."""
 
-    _fields_ = [("ws", c_void_p), ("variant", c_int), ("host_in", c_void_p), ("host_out", c_void_p)]
+    _fields_ = [("ws", c_void_p), ("variant", c_int), ("host_in", c_void_p), ("host_out", c_void_p),
+                ("batch", c_int), ("no_flush", c_int)]
 
 
 def dims_array(dims) -> ctypes.Array:

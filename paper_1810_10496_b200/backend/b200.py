@@ -15,9 +15,19 @@ backend/toolchain.py:276-307`) behind the ABC of `backend/types.py:121-152`:
   input, generated on the device (the ``<validation_input>#n`` descriptor of
   toolchain.py:231-233).
 * ``measurement_lock``: one lock per backend, and one backend per device.
+* ``prefetch(kernel, orders)`` / ``prefetch_many(jobs)``: the fresh
+  evaluations ``explore`` is about to perform (the first order of every
+  distinct digest, explorer.py:175-190) run as ONE device batch
+  (``pf_eval_batch``): validation runs with their outputs copied back and
+  the timed measurement samples, back to back on one stream.  ``execute``
+  then serves those calls from the batch's results, so the engine's record
+  stream is unchanged (same calls, same order) while the device never waits
+  for the host between candidates.
 
 Error mapping: a CUDA failure returns ``CRASH`` and resets the
-device; a run slower than ``set_timeout_override`` returns ``TIMEOUT``
+device -- unless torch shares the CUDA context in this process (NCCL groups,
+tensors), where a reset would destroy them: the backend is then marked
+failed and later calls raise ``BackendError``; a run slower than ``set_timeout_override`` returns ``TIMEOUT``
 (toolchain.py:250-258 kills the runner; an in-process kernel cannot be
 killed, so every variant is bounded by construction); configuration errors
 raise ``BackendError``.  There is no CPU path: without libpfgpu.so this module
@@ -26,10 +36,12 @@ does not import.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import gzip
 import json
 import statistics
+import sys
 from collections import OrderedDict
 from ctypes import byref, c_double, c_float, c_int, c_int64, c_void_p
 from pathlib import Path
@@ -225,6 +237,43 @@ def alg_work(bench: str, dims) -> tuple[float, float]:
     return b.value, f.value
 
 
+def _eval_item(ws: Workspace, variant: int, batch: int = 1, no_flush: bool = True, host_out=None):
+    it = _abi.PfEval()
+    it.ws, it.variant, it.batch, it.no_flush = ws.handle, variant, batch, int(no_flush)
+    it._keep = host_out  # the pointer table must outlive the batch
+    if host_out is not None:
+        it.host_out = ctypes.cast(host_out, c_void_p)
+    return it
+
+
+class _Staging:
+    """A pinned host buffer (pf_host_alloc) reused across batches."""
+
+    def __init__(self, lib, size: int):
+        self.lib = lib
+        p = c_void_p()
+        _abi.check(lib.pf_host_alloc(size, byref(p)))
+        self.ptr, self.size, self.busy = p.value, size, False
+
+    def release(self) -> None:
+        self.busy = False
+
+    def free(self) -> None:
+        if self.ptr:
+            self.lib.pf_host_free(self.ptr)
+            self.ptr = None
+
+
+def _torch_shares_context() -> bool:
+    """True when torch has initialised CUDA in this process (its tensors and
+    NCCL communicators live in the same primary context as libpfgpu's)."""
+    torch = sys.modules.get("torch")
+    try:
+        return bool(torch is not None and torch.cuda.is_initialized())
+    except Exception:  # noqa: BLE001 -- a broken torch import means no shared context
+        return False
+
+
 def device_count() -> int:
     n = c_int()
     rc = _abi.lib().pf_device_count(byref(n))
@@ -272,6 +321,20 @@ class B200Backend(Backend):
         # code -> identical performance", the premise of explorer.py:175-183);
         # off by default so final_reps averages independent runs.
         self.measurement_cache: dict | None = None
+        # pure-function memos: compile is pure in (kernel, order)
+        self._variant_memo: dict[tuple, int] = {}
+        self._supported_memo: dict[tuple, bool] = {}
+        self._compile_memo: dict[tuple, object] = {}
+        # results of the last prefetch, consumed by execute():
+        # (digest, "validation"|"measurement", input descriptor) -> (ms, outputs | None)
+        self._prefetched: dict[tuple, tuple] = {}
+        self._pending: list = []        # [(future, keys, job)] in submission order
+        self._pending_keys: dict = {}   # key -> future of the batch that will produce it
+        self._staging_pool: list = []
+        self._worker = None
+        self.failed: str | None = None
+        self.prefetch_batches = 0
+        self.batch_ms = 0.0
 
     # ------------------------------------------------------------ helpers
     def set_timeout_override(self, kernel_id: str, timeout: float) -> None:
@@ -282,9 +345,14 @@ class B200Backend(Backend):
 
     def variant_for(self, kernel: KernelCase, order) -> tuple[str, int]:
         bench = registry.bench_of(kernel)
-        if not isinstance(order, PhaseOrder):  # a foreign (reference) PhaseOrder: same pass names
-            order = PhaseOrder(tuple(PassId(p.name) for p in order.passes))
-        return bench, family(bench).select(passmodel.interpret(order))
+        key = (bench, tuple(p.name for p in order.passes))
+        v = self._variant_memo.get(key)
+        if v is None:
+            if not isinstance(order, PhaseOrder):  # a foreign (reference) PhaseOrder: same pass names
+                order = PhaseOrder(tuple(PassId(p.name) for p in order.passes))
+            v = family(bench).select(passmodel.interpret(order))
+            self._variant_memo[key] = v
+        return bench, v
 
     def artifact(self, bench: str, variant: int):
         key = (bench, variant)
@@ -318,31 +386,75 @@ class B200Backend(Backend):
             w.close()
 
     def close(self) -> None:
+        self._drain()
+        if self._worker is not None:
+            self._worker.shutdown()
+            self._worker = None
         for w in self._ws.values():
             w.close()
         self._ws.clear()
+        for st in self._staging_pool:
+            st.free()
+        self._staging_pool.clear()
 
     def _crash(self, exc: _abi.PfError):
-        # A sticky CUDA error poisons the context: drop every workspace and reset.
+        # A sticky CUDA error poisons the context: drop every workspace and reset
+        # -- unless torch shares the primary context (a reset would destroy its
+        # tensors and NCCL communicators): then the backend is marked failed.
+        self._prefetched.clear()
+        self._pending.clear()
+        self._pending_keys.clear()
+        if _torch_shares_context():
+            self.failed = str(exc)
+            return self.T.ExecutionOutcome(self.T.ExecutionStatus.CRASH, log=str(exc) + " (device left failed)")
         for w in self._ws.values():
             w.handle = None  # memory dies with the context
+            w.warm.clear()
         self._ws.clear()
+        for st in self._staging_pool:
+            st.ptr = None  # pinned memory dies with the context
+        self._staging_pool.clear()
         self.lib.pf_device_reset(self.device)
         return self.T.ExecutionOutcome(self.T.ExecutionStatus.CRASH, log=str(exc))
 
     def _supported(self, bench: str, variant: int, dims) -> bool:
-        return _supported_dims(bench, variant, dims)
+        key = (bench, variant, tuple(dims))
+        ok = self._supported_memo.get(key)
+        if ok is None:
+            ok = self._supported_memo[key] = _supported_dims(bench, variant, dims)
+        return ok
+
+    @contextlib.contextmanager
+    def digest_timing(self):
+        """Inside the block, measurements are keyed by artifact digest: an
+        artifact measured once keeps that time (identical machine code ->
+        identical performance, the premise of REUSED, explorer.py:175-183).
+        Used around reduce_order, whose trials mostly re-measure the same
+        artifact and would otherwise be rejected by run-to-run noise."""
+        was = self.measurement_cache
+        self.measurement_cache = {} if was is None else was
+        try:
+            yield
+        finally:
+            self.measurement_cache = was
 
     # ------------------------------------------------------------ Backend API
     def compile(self, kernel: KernelCase, order):
         bench, variant = self.variant_for(kernel, order)
+        key = (bench, variant, kernel.validation_input, kernel.measurement_input)
+        out = self._compile_memo.get(key)
+        if out is not None:
+            return out
+        out = self.T.CompileOutcome.success(self.artifact(bench, variant))
         for text in (kernel.validation_input, kernel.measurement_input):
             _, dims = registry.parse_descriptor(text)
             if not self._supported(bench, variant, dims):
-                return self.T.CompileOutcome.codegen_failure(
+                out = self.T.CompileOutcome.codegen_failure(
                     f"{bench} variant {family(bench).key(variant)} does not support {text}"
                 )
-        return self.T.CompileOutcome.success(self.artifact(bench, variant))
+                break
+        self._compile_memo[key] = out
+        return out
 
     def execute(
         self,
@@ -363,7 +475,22 @@ class B200Backend(Backend):
                         random_input_index: int | None = None):
         """``execute`` after the order -> variant lookup (also the entry of the
         process-level runner, ``pftool run``)."""
+        if self.failed:
+            raise self.T.BackendError(f"device {self.device} failed earlier: {self.failed}")
         artifact = self.artifact(bench, variant)
+        if random_input_index is None and (self._prefetched or self._pending):
+            kind = input_kind.value
+            desc = kernel.validation_input if kind == "validation" else kernel.measurement_input
+            key = (artifact.digest, kind, desc)
+            if key in self._pending_keys:
+                self._wait_for(key)
+            else:
+                self._drain()  # no device work of this backend may overlap a batch
+            hit = self._prefetched.pop(key, None)
+            if hit is not None:
+                return self._finish(kernel, hit[0], hit[1])
+        elif self._pending:
+            self._drain()
         try:
             # compare by value: the caller may use the reference's InputKind enum
             if random_input_index is not None or input_kind.value == "validation":
@@ -424,6 +551,207 @@ class B200Backend(Backend):
         ms = ws.run(variant, samples=samples, batch=batch, restore=True, flush=self.flush_l2)
         self._count(ws.bench, variant, ws.dims, samples * batch)
         return ms
+
+    # ------------------------------------------------------------ batched evaluation
+    def prefetch(self, kernel: KernelCase, orders) -> int:
+        """``explore(..., prefetch=True)`` hook: batch the fresh evaluations of
+        ``orders`` (see module doc).  Returns the number of candidates."""
+        return self.prefetch_many([(kernel, orders)])
+
+    def fresh_candidates(self, kernel: KernelCase, orders) -> list[tuple[str, int, str]]:
+        """(bench, variant, digest) of the first order of every distinct
+        digest in ``orders`` that compiles -- explore's fresh evaluations."""
+        out, seen = [], set()
+        for order in orders:
+            c = self.compile(kernel, order)
+            if not c.is_ok or c.artifact.digest in seen:
+                continue
+            seen.add(c.artifact.digest)
+            bench, variant = self.variant_for(kernel, order)
+            out.append((bench, variant, c.artifact.digest))
+        return out
+
+    def prefetch_many(self, jobs, host_inputs: dict | None = None) -> int:
+        """Run the fresh evaluations of several (kernel, orders) jobs as
+        device batches, one per job, issued by a worker thread so that the
+        host prepares job k+1 (and the engine walks job k's records) while
+        the device runs job k.  Per candidate: one validation run on the
+        stock validation input (outputs copied back) and the measurement
+        protocol of ``execute`` (first use: two warm-up runs that size the
+        batch of us-scale kernels; then ``samples`` timed samples, each after
+        an L2 flush; median).  ``host_inputs`` maps (kernel id, "validation"
+        | "measurement") to {array index: pinned host pointer}: those inputs
+        are uploaded first, asynchronously on the copy stream (the end-to-end
+        path).  ``execute`` waits for a job's batch only when it asks for
+        one of that job's results.  A CUDA failure inside a batch drops the
+        remaining results (the engine then evaluates candidate by candidate,
+        which isolates the failing one as a CRASH record).  Returns the
+        number of candidates."""
+        if self.failed:
+            raise self.T.BackendError(f"device {self.device} failed earlier: {self.failed}")
+        self._drain()
+        host_inputs = host_inputs or {}
+        total = 0
+        try:
+            for (kid, kind), table in host_inputs.items():
+                kernel = next(k for k, _ in jobs if k.id == kid)
+                _, dims = registry.parse_descriptor(
+                    kernel.validation_input if kind == "validation" else kernel.measurement_input)
+                ws = self.workspace(registry.bench_of(kernel), dims, True, -1)
+                for a, ptr in sorted(table.items()):
+                    _abi.check(self.lib.pf_ws_upload_async(ws.handle, a, ptr, ws.elems[a]))
+                # the uploaded arrays ARE this descriptor's input (the runner's
+                # data file); a later generate() for it is a no-op
+                ws.input_tag = (True, int(self.seed), -1)
+            for kernel, orders in jobs:
+                total += self._submit_job(kernel, orders)
+        except _abi.PfError as exc:
+            return self._batch_failed(exc) or total
+        return total
+
+    def _submit_job(self, kernel: KernelCase, orders) -> int:
+        cands = self.fresh_candidates(kernel, orders)
+        if not cands:
+            return 0
+        _, vdims = registry.parse_descriptor(kernel.validation_input)
+        _, mdims = registry.parse_descriptor(kernel.measurement_input)
+        plan = [(bench, variant, digest, self.workspace(bench, vdims, True, -1),
+                 self.workspace(bench, mdims, True, -1)) for bench, variant, digest in cands]
+        # first use of a measurement variant: warm-up runs decide the batch size
+        cold = []
+        for bench, variant, digest, vws, mws in plan:
+            if variant not in mws.warm and (mws, variant) not in cold:
+                cold.append((mws, variant))
+        if cold:
+            ms = self._worker_submit([_eval_item(ws, v) for ws, v in cold for _ in range(2)]).result()
+            for i, (ws, variant) in enumerate(cold):
+                key = (ws.bench, ws.dims, variant)
+                first = ms[2 * i + 1]
+                ws.warm.add(variant)
+                self._first_ms[key] = first
+                self._count(ws.bench, variant, ws.dims, 2)
+                if key not in self._batch:
+                    self._batch[key] = (min(self.max_batch, max(1, int(self.min_sample_ms / max(first, 1e-4)) + 1))
+                                        if first < self.min_sample_ms else 1)
+        out_n = [sum(n for (_, _, o), n in zip(vws.arrays, vws.elems) if o) for _, _, _, vws, _ in plan]
+        staging = self._staging_buffer(4 * sum(out_n))
+        items, layout, off = [], [], 0
+        for (bench, variant, digest, vws, mws), nout in zip(plan, out_n):
+            ptrs, o = [], off
+            for (_, _, is_out), n in zip(vws.arrays, vws.elems):
+                ptrs.append(staging.ptr + o if is_out else None)
+                o += 4 * n if is_out else 0
+            items.append(_eval_item(vws, variant, host_out=(c_void_p * len(vws.arrays))(*ptrs)))
+            entry = {"v": len(items) - 1, "off": off // 4, "n": nout, "m": []}
+            off = o
+            if not (self.measurement_cache is not None and (kernel.measurement_input, digest) in self.measurement_cache):
+                key = (bench, mws.dims, variant)
+                samples = 1 if self._first_ms.get(key, 0.0) > self.slow_ms else self.samples
+                for _ in range(samples):
+                    items.append(_eval_item(mws, variant, batch=self._batch.get(key, 1), no_flush=not self.flush_l2))
+                    entry["m"].append(len(items) - 1)
+            layout.append(entry)
+        future = self._worker_submit(items)
+        keys = []
+        for (bench, variant, digest, vws, mws) in plan:
+            keys += [(digest, "validation", kernel.validation_input), (digest, "measurement", kernel.measurement_input)]
+        self._pending.append((future, keys, (kernel, plan, layout, staging)))
+        for k in keys:
+            self._prefetched.pop(k, None)
+            self._pending_keys[k] = future
+        return len(plan)
+
+    def _collect(self, future, job) -> None:
+        """Turn one finished batch into prefetched execute() results."""
+        kernel, plan, layout, staging = job
+        ms = future.result()
+        import numpy as np
+
+        for (bench, variant, digest, vws, mws), entry in zip(plan, layout):
+            values = tuple(np.ctypeslib.as_array(
+                (ctypes.c_float * max(1, entry["n"])).from_address(staging.ptr + 4 * entry["off"]))[:entry["n"]].tolist())
+            self._prefetched[(digest, "validation", kernel.validation_input)] = (ms[entry["v"]], values)
+            self._count(bench, variant, vws.dims, 1)
+            ckey = (kernel.measurement_input, digest)
+            if entry["m"]:
+                key = (bench, mws.dims, variant)
+                t = statistics.median(ms[i] for i in entry["m"])
+                self._count(bench, variant, mws.dims, len(entry["m"]) * self._batch.get(key, 1))
+                if self.measurement_cache is not None:
+                    self.measurement_cache[ckey] = t
+            else:
+                t = self.measurement_cache[ckey]
+            self._prefetched[(digest, "measurement", kernel.measurement_input)] = (t, None)
+        staging.release()
+        self.prefetch_batches += 1
+
+    def _wait_for(self, key) -> None:
+        """Block until the batch holding ``key`` (and every earlier one) is done."""
+        future = self._pending_keys.get(key)
+        if future is None:
+            return
+        while self._pending:
+            f, keys, job = self._pending.pop(0)
+            for k in keys:
+                self._pending_keys.pop(k, None)
+            try:
+                self._collect(f, job)
+            except _abi.PfError as exc:
+                self._batch_failed(exc)
+                return
+            if f is future:
+                return
+
+    def _drain(self) -> None:
+        while self._pending:
+            self._wait_for(self._pending[0][1][0])
+
+    def _batch_failed(self, exc: "_abi.PfError") -> int:
+        for f, _, _ in self._pending:
+            try:
+                f.result()
+            except Exception:  # noqa: BLE001 -- the batch after a failed one is dropped too
+                pass
+        self._pending.clear()
+        self._pending_keys.clear()
+        self._prefetched.clear()
+        if exc.code != _abi.PF_ECUDA:
+            raise self.T.BackendError(str(exc)) from exc
+        self._crash(exc)
+        if self.failed:
+            raise self.T.BackendError(f"device {self.device} failed: {exc}") from exc
+        return 0
+
+    def _worker_submit(self, items):
+        """Enqueue one pf_eval_batch on the backend's device worker (a single
+        thread: batches never overlap on the device; ctypes drops the GIL)."""
+        if self._worker is None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            self._worker = ThreadPoolExecutor(max_workers=1, thread_name_prefix=f"pfgpu-dev{self.device}")
+        arr = (_abi.PfEval * len(items))(*items)
+        keep = [it._keep for it in items]
+
+        def run():
+            n = len(items)
+            ms = (c_float * n)()
+            total = c_float()
+            _abi.check(self.lib.pf_eval_batch(arr, n, 1, 1, ms, byref(total)))
+            self.batch_ms += total.value
+            return list(ms)
+
+        return self._worker.submit(run)
+
+    def _staging_buffer(self, nbytes: int) -> "_Staging":
+        """Pinned host staging for one batch's validation outputs (pooled)."""
+        for st in self._staging_pool:
+            if not st.busy and st.size >= nbytes:
+                st.busy = True
+                return st
+        st = _Staging(self.lib, max(nbytes, 1 << 20))
+        st.busy = True
+        self._staging_pool.append(st)
+        return st
 
     # ------------------------------------------------------------ conveniences
     def baseline_outputs(self, kernel: KernelCase) -> tuple[float, ...]:

@@ -86,7 +86,7 @@ int flush_l2(int device, cudaStream_t s) {
   // one L2 of write-backs inside its own measurement.
   PF_CUDA(cudaMemsetAsync(fb->ptr, 0x5a, fb->bytes, s));
   const int64_t n4 = (int64_t)(fb->bytes / sizeof(float4));
-  flush_read_kernel<<<4 * 148, 512, 0, s>>>(reinterpret_cast<const float4*>(fb->ptr), n4,
+  flush_read_kernel<<<4 * device_sms(), 512, 0, s>>>(reinterpret_cast<const float4*>(fb->ptr), n4,
                                             reinterpret_cast<float*>(fb->ptr));
   PF_CUDA(cudaGetLastError());
   return PF_OK;
@@ -179,12 +179,71 @@ void register_bench(int id, const BenchDesc* desc) {
   if (id >= 0 && id < B_COUNT) registry()[id] = desc;
 }
 
-int* Workspace::ensure_tile_flags() {
+int* Workspace::ensure_tile_flags(cudaStream_t s) {
   if (tile_flags) return tile_flags;
   if (cudaMalloc(&tile_flags, kTileFlags * sizeof(int)) != cudaSuccess) return tile_flags = nullptr;
-  cudaMemset(tile_flags, 0, kTileFlags * sizeof(int));  // first use is outside timed regions (warm-up)
+  // on the launch stream: ordered before the first kernel that waits on a flag
+  cudaMemsetAsync(tile_flags, 0, kTileFlags * sizeof(int), s);
   tile_epoch = 0;
   return tile_flags;
+}
+
+// ---------------------------------------------------------------- per-context function setup
+namespace {
+std::mutex g_attr_mu;
+int g_ctx_gen[64];  // bumped by pf_device_reset
+struct AttrKey {
+  const void* fn;
+  int device, gen;
+  bool operator==(const AttrKey& o) const { return fn == o.fn && device == o.device && gen == o.gen; }
+};
+struct AttrHash {
+  size_t operator()(const AttrKey& k) const {
+    return std::hash<const void*>()(k.fn) ^ ((size_t)k.device << 48) ^ ((size_t)k.gen << 32);
+  }
+};
+std::unordered_map<AttrKey, int, AttrHash> g_smem_set;    // -> bytes set
+std::unordered_map<AttrKey, int, AttrHash> g_occupancy;   // -> CTAs per SM
+int g_sms[64];
+}  // namespace
+
+void set_smem_attr(const void* fn, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  const AttrKey k{fn, dev, g_ctx_gen[dev & 63]};
+  auto it = g_smem_set.find(k);
+  if (it != g_smem_set.end() && it->second >= bytes) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  g_smem_set[k] = bytes;
+}
+
+int device_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int& n = g_sms[dev & 63];
+  if (!n && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  return n;
+}
+
+void note_context_reset(int dev) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  ++g_ctx_gen[dev & 63];
+}
+
+int occupancy(const void* fn, int threads, size_t smem) {
+  set_smem_attr(fn, (int)smem);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  const AttrKey k{fn, dev, g_ctx_gen[dev & 63]};
+  auto it = g_occupancy.find(k);
+  if (it != g_occupancy.end()) return it->second;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) per_sm = 0;
+  g_occupancy[k] = per_sm;
+  return per_sm;
 }
 
 float* Workspace::ensure_aux(size_t bytes) {
@@ -260,6 +319,7 @@ int pf_device_reset(int device) {
   int rc = set_device(device);
   if (rc) return rc;
   PF_CUDA(cudaDeviceReset());
+  pf::note_context_reset(device);  // function attributes died with the context
   return PF_OK;
 }
 
@@ -453,6 +513,29 @@ int pf_ws_upload(pf_ws* ws, int array, const float* host, int64_t n) {
   return PF_OK;
 }
 
+int pf_ws_upload_async(pf_ws* ws, int array, const float* host, int64_t n) {
+  if (array < 0 || array >= ws->desc->narrays) return fail(PF_EINVAL, "array index out of range");
+  if (n != ws->elems[array]) return fail(PF_EINVAL, "element count mismatch");
+  if (int rc = set_device(ws->device)) return rc;
+  cudaStream_t cs = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_flush_mu);
+    if (!g_copy_stream[ws->device])
+      PF_CUDA(cudaStreamCreateWithFlags(&g_copy_stream[ws->device], cudaStreamNonBlocking));
+    cs = g_copy_stream[ws->device];
+  }
+  // copy after everything already enqueued on the workspace, and everything
+  // enqueued on the workspace afterwards after the copy
+  PF_CUDA(cudaEventRecord(ws->ev0, ws->stream));
+  PF_CUDA(cudaStreamWaitEvent(cs, ws->ev0, 0));
+  PF_CUDA(cudaMemcpyAsync(ws->a.p[array], host, n * sizeof(float), cudaMemcpyHostToDevice, cs));
+  if (ws->pristine[array])
+    PF_CUDA(cudaMemcpyAsync(ws->pristine[array], ws->a.p[array], n * sizeof(float), cudaMemcpyDeviceToDevice, cs));
+  PF_CUDA(cudaEventRecord(ws->ev1, cs));
+  PF_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev1, 0));
+  return PF_OK;
+}
+
 int pf_ws_download(pf_ws* ws, int array, float* host, int64_t n) {
   if (array < 0 || array >= ws->desc->narrays) return fail(PF_EINVAL, "array index out of range");
   if (n != ws->elems[array]) return fail(PF_EINVAL, "element count mismatch");
@@ -552,18 +635,30 @@ int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush, float* ms
     if (!ws || ws->device != device) return fail(PF_EINVAL, "batch workspaces must share one device");
     if (evals[i].variant < 0 || evals[i].variant >= ws->desc->nvariants)
       return fail(PF_EINVAL, "variant index out of range");
+    if (evals[i].batch < 0 || evals[i].batch > 1 << 16) return fail(PF_EINVAL, "batch out of range");
     if (ws->desc->check && ws->desc->check(evals[i].variant, ws->dims) != 0)
       return fail(PF_EINVAL, "variant does not support these dims");
   }
   if (int rc = set_device(device)) return rc;
-  // Everything goes on the first workspace's stream; the others must be idle.
-  for (int i = 0; i < n; ++i) PF_CUDA(cudaStreamSynchronize(evals[i].ws->stream));
+  // Everything goes on the first workspace's stream, ordered after the work
+  // already enqueued on every workspace's own stream (e.g. pf_ws_upload_async
+  // copies) without blocking the host.
   cudaStream_t st = evals[0].ws->stream;
   thread_local std::vector<cudaEvent_t> pool;
-  while ((int)pool.size() < 3 * n + 2) {
+  while ((int)pool.size() < 4 * n + 2) {
     cudaEvent_t e;
     PF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
     pool.push_back(e);
+  }
+  {
+    std::vector<cudaStream_t> joined{st};
+    for (int i = 0; i < n; ++i) {
+      cudaStream_t ws_st = evals[i].ws->stream;
+      if (std::find(joined.begin(), joined.end(), ws_st) != joined.end()) continue;
+      joined.push_back(ws_st);
+      PF_CUDA(cudaEventRecord(pool[3 * n + 2 + i], ws_st));
+      PF_CUDA(cudaStreamWaitEvent(st, pool[3 * n + 2 + i], 0));
+    }
   }
   cudaEvent_t first = pool[2 * n], last = pool[2 * n + 1];
   PF_CUDA(cudaEventRecord(first, st));
@@ -624,12 +719,14 @@ int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush, float* ms
           PF_CUDA(cudaMemsetAsync(ws->a.p[a], 0, bytes, st));
       }
     }
-    if (flush)
+    if (flush && !evals[i].no_flush)
       if (int rc = flush_l2(device, st)) return rc;
     PF_CUDA(cudaEventRecord(pool[2 * i], st));
-    d->run[evals[i].variant](*ws, st);
-    PF_CUDA(cudaGetLastError());
-    if (const char* why = take_launch_error()) return fail(PF_ECUDA, why);
+    for (int b = 0; b < std::max(1, evals[i].batch); ++b) {
+      d->run[evals[i].variant](*ws, st);
+      PF_CUDA(cudaGetLastError());
+      if (const char* why = take_launch_error()) return fail(PF_ECUDA, why);
+    }
     PF_CUDA(cudaEventRecord(pool[2 * i + 1], st));
     if (evals[i].host_out) {
       for (int a = 0; a < d->narrays; ++a)
@@ -643,7 +740,7 @@ int pf_eval_batch(const pf_eval* evals, int n, int restore, int flush, float* ms
   for (int i = 0; i < n; ++i) {
     float t = 0.f;
     PF_CUDA(cudaEventElapsedTime(&t, pool[2 * i], pool[2 * i + 1]));
-    if (ms_each) ms_each[i] = t;
+    if (ms_each) ms_each[i] = t / std::max(1, evals[i].batch);
   }
   float tot = 0.f;
   PF_CUDA(cudaEventElapsedTime(&tot, first, last));
@@ -667,7 +764,7 @@ int pf_compare(pf_ws* test, pf_ws* ref, double rtol, double atol_rel, double* ma
     if (!d->arrays[a].is_output) continue;
     int64_t n = test->elems[a];
     cudaMemsetAsync(dev, 0, 16, test->stream);
-    unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, device_sms() * 8);
     if (blocks < 1) blocks = 1;
     absmax_kernel<<<blocks, 256, 0, test->stream>>>(ref->a.p[a], n, dev);
     compare_kernel<<<blocks, 256, 0, test->stream>>>(test->a.p[a], ref->a.p[a], n, rtol, dev, atol_rel,
@@ -699,7 +796,7 @@ int pf_checksum(pf_ws* ws, int array, double* sum, double* abs_sum) {
   PF_CUDA(cudaMalloc(&dev, 16));
   cudaMemsetAsync(dev, 0, 16, ws->stream);
   int64_t n = ws->elems[array];
-  unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+  unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, device_sms() * 8));
   checksum_kernel<<<blocks, 256, 0, ws->stream>>>(ws->a.p[array], n, dev);
   double h[2];
   cudaError_t e = cudaMemcpyAsync(h, dev, 16, cudaMemcpyDeviceToHost, ws->stream);

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) s1_col_dot(const float* __restrict__ A, i
 template <BenchId Bn, int V, int kUnroll, int kVec>
 inline void launch_s1_row_dot(const float* A, int lda, const float* v, int n, int rows, const float* init, float* out,
                               cudaStream_t s) {
-  int blocks = (int)std::min<int64_t>(((int64_t)rows + 7) / 8, 148 * 16);
+  int blocks = (int)std::min<int64_t>(((int64_t)rows + 7) / 8, device_sms() * 16);
   s1_row_dot<Bn, V, kUnroll, kVec><<<blocks, 256, 0, s>>>(A, lda, v, n, rows, init, out);
 }
 
@@ -154,7 +154,7 @@ template <BenchId Bn, int V, int kUnroll, int kVec>
 inline void launch_s1_col_dot(const float* A, int lda, const float* v, int m, int cols, float* out, cudaStream_t s) {
   constexpr int W = kVec ? 4 : 1;
   const int gx = (int)cdiv(cols, 256 * W);
-  int splits = (int)cdiv(148 * 4, gx);
+  int splits = (int)cdiv(device_sms() * 4, gx);
   splits = std::max(1, std::min(splits, (m + 63) / 64));
   const int rps = (int)cdiv(m, splits);
   splits = (int)cdiv(m, rps);
@@ -327,12 +327,8 @@ inline bool fused_supported(int64_t rows, int64_t cols) {
 template <BenchId Bn, int V, int C4>
 inline void launch_fused_c4(const FusedArgs& p, cudaStream_t s) {
   const size_t smem = (size_t)kFusedStages * p.cols * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(s2_fused<Bn, V, C4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
-  int grid = std::min(p.rows, 148);
+  set_smem_attr((const void*)s2_fused<Bn, V, C4>, 200 * 1024);
+  int grid = std::min(p.rows, device_sms());
   s2_fused<Bn, V, C4><<<grid, kFusedThreads, smem, s>>>(p);
 }
 

@@ -166,7 +166,7 @@ __global__ void set_unit_diag(float* sym, int m) {
 template <BenchId Bn, int V, int kPass>
 inline void launch_colstat(const float* data, const float* mean, float* out, int m, int n, cudaStream_t s) {
   const int gx = (int)cdiv(m, 256);
-  int splits = std::max(1, std::min((int)cdiv(148 * 4, gx), (n + 31) / 32));
+  int splits = std::max(1, std::min((int)cdiv(device_sms() * 4, gx), (n + 31) / 32));
   const int rps = (int)cdiv(n, splits);
   splits = (int)cdiv(n, rps);
   colsum_split<Bn, V, kPass><<<dim3(gx, splits), 256, 0, s>>>(data, mean, out, m, n, rps);
@@ -294,7 +294,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
       TcGemmArgs g{m, m, n, 1.f, 0.f, xt, np, false, xt, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
       g.Alo = xt_lo;
       g.Blo = xt_lo;
-      g.tile_flags = ws.ensure_tile_flags();
+      g.tile_flags = ws.ensure_tile_flags(s);
       g.epoch = ++ws.tile_epoch;
       if (!launch_tc_tma<Bn, V>(g, s)) {
         launch_failed("CORR/COVAR stage 2: TMA operand maps rejected");

@@ -375,15 +375,8 @@ inline int c3_mode() {
 
 template <int V>
 void launch_s2(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s) {
-  static int grid = 0;
-  if (!grid) {
-    cudaFuncSetAttribute(conv3d_s2<B_3DCONV, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kNS * kSlotBytes));
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv3d_s2<B_3DCONV, V>, kS2Threads, kNS * kSlotBytes);
-    grid = std::max(1, per_sm) * sms;
-  }
+  const int grid =
+      std::max(1, occupancy((const void*)conv3d_s2<B_3DCONV, V>, kS2Threads, kNS * kSlotBytes)) * device_sms();
   S2Params p;
   if (!tma::make_map_3d(&p.map, A, nk, nj, ni, kBoxK, kBoxJ, 1)) {  // check() guarantees nk % 4 == 0
     launch_failed("3DCONV stage 2: cuTensorMapEncodeTiled rejected the input plane map");

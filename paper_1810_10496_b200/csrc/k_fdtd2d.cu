@@ -296,11 +296,7 @@ void tb_sequence(Workspace& ws, cudaStream_t s) {
     return;
   }
   float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(step_tb<Bn, V, kTB, kTR, kTBThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  set_smem_attr((const void*)step_tb<Bn, V, kTB, kTR, kTBThreads>, (int)smem);
   const dim3 grid(cdiv(ny, kTT), cdiv(nx, kTT));
   int launches = 0;
   for (int t = 0; t < tmax; t += kTB, ++launches) {
@@ -320,18 +316,22 @@ void tb_sequence(Workspace& ws, cudaStream_t s) {
 // thread's own registers, and across warps from one shared row per warp and
 // field (hz's last row before the ey/ex phase, ey's first row before the hz
 // phase): two block barriers per time step and no per-cell shared-memory
-// traffic.  kRT steps per launch; halo kRT rows and one float4 of columns, so
-// the CTA writes rows kRT .. 31-kRT and columns 4 .. 123.
+// traffic.  kRT steps per launch.  A region edge is wrong after one step and
+// the error advances one row and one column per step (ey/hz couple rows i-1/i+1,
+// ex/hz columns j-1/j+1), so the halo is kRT rows and kH = ceil(kRT/4) float4s
+// of columns per side: the CTA writes rows kRT .. kRows-1-kRT and lanes
+// kH .. 31-kH, i.e. 128 - 8*kH columns per column tile.
 template <BenchId Bn, int V, int kRT, int kW>
 __global__ void __launch_bounds__(32 * kW) step_rt(const float* __restrict__ fict, const float* __restrict__ ex0,
                                                const float* __restrict__ ey0, const float* __restrict__ hz0,
                                                float* __restrict__ ex1, float* __restrict__ ey1,
                                                float* __restrict__ hz1, int nx, int ny, int t0, int steps) {
   constexpr int kR = 8, kRows = kR * kW, kOutRows = kRows - 2 * kRT;
+  constexpr int kH = (kRT + 3) / 4, kCols = 128 - 8 * kH;
   __shared__ float4 hz_last[kW][32], ey_first[kW][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gi0 = blockIdx.y * kOutRows - kRT + warp * kR;  // global row of this thread's r = 0
-  const int gj = blockIdx.x * 120 - 4 + 4 * lane;          // global column of this thread's c = 0
+  const int gj = blockIdx.x * kCols - 4 * kH + 4 * lane;   // global column of this thread's c = 0
   const bool col_in = gj >= 0 && gj < ny;                    // ny % 4 == 0: a float4 is all in or all out
   float ex[kR][4], ey[kR][4], hz[kR][4];
 #pragma unroll
@@ -387,8 +387,8 @@ __global__ void __launch_bounds__(32 * kW) step_rt(const float* __restrict__ fic
       }
     }
   }
-  // ---- store rows kRT .. 31-kRT of the region, lanes 1 .. 30
-  if (lane == 0 || lane == 31 || !col_in) return;
+  // ---- store rows kRT .. kRows-1-kRT of the region, lanes kH .. 31-kH
+  if (lane < kH || lane > 31 - kH || !col_in) return;
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
     const int lr = warp * kR + r, gi = gi0 + r;
@@ -410,7 +410,8 @@ void rt_sequence(Workspace& ws, cudaStream_t s) {
     return;
   }
   float* buf[2][3] = {{ws.a.p[1], ws.a.p[2], ws.a.p[3]}, {scratch, scratch + n, scratch + 2 * n}};
-  const dim3 grid(cdiv(ny, 120), cdiv(nx, 8 * kW - 2 * kRT));
+  constexpr int kCols = 128 - 8 * ((kRT + 3) / 4);
+  const dim3 grid(cdiv(ny, kCols), cdiv(nx, 8 * kW - 2 * kRT));
   int launches = 0;
   for (int t = 0; t < tmax; t += kRT, ++launches) {
     float** src = buf[launches & 1];
@@ -423,13 +424,14 @@ void rt_sequence(Workspace& ws, cudaStream_t s) {
 }
 
 // Stage 2 = the register-tiled temporal blocking (kRTSteps time steps per
-// launch on 64-row x 128-column register regions, 8 warps): 2.09 ms for
-// 2048^2 x 500 steps vs 5.77 ms for the shared-memory blocking (64x64
-// regions, 4 steps; PF_FDTD_TB=4) and 6.16 ms for the per-step fused sequence
-// (PF_FDTD_TB=0).  Register-tiled shapes measured and dropped: 4 warps x 4-6
-// steps (2.37-2.62 ms), 8 warps x 5/7/8 steps (2.15-2.33 ms), 16 warps x
-// 8/10/12 steps (2.04-2.45 ms; 12 steps ties at one 512-thread CTA per SM).
-constexpr int kRTSteps = 6, kRTWarps = 8;
+// launch on (8*kRTWarps)-row x 128-column register regions).  Measured on
+// B200 for 2048^2 x 500 steps with the ceil(steps/4)-float4 column halo
+// (round 2; round 1's one-float4 halo was only correct up to 4 steps): 4/6/8/
+// 10/12 steps x 8 warps 2.81/2.32/2.12/-/- ms, 8/10/12 steps x 16 warps
+// 2.50/2.20/2.06 ms; the shared-memory blocking (64x64 regions, 4 steps,
+// PF_FDTD_TB=4) 5.77 ms and the per-step fused sequence (PF_FDTD_TB=0)
+// 6.16 ms.
+constexpr int kRTSteps = 12, kRTWarps = 16;
 inline int fdtd_tb_depth() {
   static const int d = [] {
     const char* e = std::getenv("PF_FDTD_TB");
@@ -438,10 +440,38 @@ inline int fdtd_tb_depth() {
   }();
   return d;
 }
+// register-tiled steps per launch and warps per CTA (A/B switches
+// PF_FDTD_RT=4|6|8|10|12, PF_FDTD_RW=8|16; defaults kRTSteps, kRTWarps)
+inline int fdtd_rt_steps() {
+  static const int d = [] {
+    const char* e = std::getenv("PF_FDTD_RT");
+    const int v = e ? std::atoi(e) : kRTSteps;
+    return (v == 4 || v == 6 || v == 8 || v == 10 || v == 12) ? v : kRTSteps;
+  }();
+  return d;
+}
+inline int fdtd_rt_warps() {
+  static const int w = [] {
+    const char* e = std::getenv("PF_FDTD_RW");
+    const int v = e ? std::atoi(e) : kRTWarps;
+    return (v == 8 || v == 16) ? v : kRTWarps;
+  }();
+  return w;
+}
+template <BenchId Bn, int V, int kW>
+cudaGraphExec_t rt_graph(Workspace& ws) {
+  switch (fdtd_rt_steps()) {
+    case 4: return cached_graph(ws, V, &rt_sequence<Bn, V, 4, kW>);
+    case 6: return cached_graph(ws, V, &rt_sequence<Bn, V, 6, kW>);
+    case 10: return cached_graph(ws, V, &rt_sequence<Bn, V, 10, kW>);
+    case 12: return cached_graph(ws, V, &rt_sequence<Bn, V, 12, kW>);
+    default: return cached_graph(ws, V, &rt_sequence<Bn, V, 8, kW>);
+  }
+}
 // time steps per stage-2 launch
 inline int fdtd_steps_per_launch() {
   const int d = fdtd_tb_depth();
-  return d == 0 ? 1 : d == 4 ? 4 : kRTSteps;
+  return d == 0 ? 1 : d == 4 ? 4 : fdtd_rt_steps();
 }
 inline bool fdtd_tb_disabled() { return fdtd_tb_depth() == 0; }
 
@@ -495,7 +525,8 @@ struct Run {
       const int d = fdtd_tb_depth();
       cudaGraphExec_t g = !tb      ? cached_graph(ws, V + 1000, &fused_sequence<B_FDTD2D, V>)
                           : d == 4 ? cached_graph(ws, V + 2000, &tb_sequence<B_FDTD2D, V, 4, 64, 256>)
-                                   : cached_graph(ws, V, &rt_sequence<B_FDTD2D, V, kRTSteps, kRTWarps>);
+                          : fdtd_rt_warps() == 16 ? rt_graph<B_FDTD2D, V, 16>(ws)
+                                                  : rt_graph<B_FDTD2D, V, 8>(ws);
       cudaGraphLaunch(g, s);
     }
   }

@@ -175,15 +175,11 @@ struct Run {
     if constexpr (K.stage == 0) {
       gesummv_s0<B_GESUMMV, V><<<cdiv(n, kB1), kB1, 0, s>>>(A, B, x, y, tmp, n);
     } else if constexpr (K.stage == 1) {
-      int blocks = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);
+      int blocks = (int)std::min<int64_t>((n + 7) / 8, device_sms() * 16);
       gesummv_s1<B_GESUMMV, V, K.unroll, K.vec><<<blocks, 256, 0, s>>>(A, B, x, y, tmp, n);
     } else {
-      static bool configured = false;
-      if (!configured) {
-        cudaFuncSetAttribute(gesummv_s2<B_GESUMMV, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-        configured = true;
-      }
-      int blocks = (int)std::min<int64_t>((n + 15) / 16, 148 * 2);
+      set_smem_attr((const void*)gesummv_s2<B_GESUMMV, V>, 100 * 1024);
+      int blocks = (int)std::min<int64_t>((n + 15) / 16, device_sms() * 2);
       gesummv_s2<B_GESUMMV, V><<<blocks, 512, n * sizeof(float), s>>>(A, B, x, y, tmp, n);
     }
   }

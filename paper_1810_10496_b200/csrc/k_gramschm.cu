@@ -166,7 +166,7 @@ void s1_sequence(Workspace& ws, cudaStream_t s) {
     const int cols = n - k - 1;
     if (cols <= 0) continue;
     const int gx = (int)cdiv(cols, 256);
-    int splits = std::max(1, std::min((int)cdiv(148 * 2, gx), (m + 127) / 128));
+    int splits = std::max(1, std::min((int)cdiv(device_sms() * 2, gx), (m + 127) / 128));
     const int rps = (int)cdiv(m, splits);
     splits = (int)cdiv(m, rps);
     gs_rrow<Bn, V><<<dim3(gx, splits), 256, 0, s>>>(A, R, Q, m, n, k, rps);
@@ -286,11 +286,7 @@ void launch_panel(Workspace& ws, cudaStream_t s) {
   float* qbuf = scratch;
   int* flags = reinterpret_cast<int*>(scratch + (size_t)n * m);
   cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), s);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gs_panel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  set_smem_attr((const void*)gs_panel<Bn, V>, 200 * 1024);
   float* A = ws.a.p[0];
   float* R = ws.a.p[1];
   float* Q = ws.a.p[2];
@@ -638,15 +634,7 @@ template <BenchId Bn, int V, int W>
 bool try_launch_panel2(void** args, int n, cudaStream_t s) {
   constexpr int NT = 16 * W;
   constexpr size_t smem = (size_t)W * kP2Rows * sizeof(float);
-  static int per_sm = -1, sms = 0;
-  if (per_sm < 0) {
-    cudaFuncSetAttribute(gs_panel2<Bn, V, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_panel2<Bn, V, W>, NT, smem) != cudaSuccess)
-      per_sm = 0;
-  }
+  const int per_sm = occupancy((const void*)gs_panel2<Bn, V, W>, NT, smem), sms = device_sms();
   const int grid = (n + W - 1) / W;
   if ((int64_t)per_sm * sms < grid) return false;  // the panels must all be co-resident
   if (cudaLaunchCooperativeKernel((const void*)gs_panel2<Bn, V, W>, dim3(grid), dim3(NT), args, smem, s) !=

@@ -108,7 +108,7 @@ struct Workspace {
   // are serialised on its stream, so epochs never interleave)
   int* tile_flags;
   int tile_epoch;
-  int* ensure_tile_flags();  // defined in abi.cu
+  int* ensure_tile_flags(cudaStream_t s);  // defined in abi.cu; zeroed on s, before the launch that uses them
   // second lazily grown buffer for data a variant hands from one launch to a
   // later one while the first scratch is reused in between (3xTF32 lo images
   // of chained products)
@@ -121,6 +121,19 @@ constexpr int kTileFlags = 4096;
 // Graph-staged variants: capture `body` once per (workspace, key) and return
 // the executable graph (abi.cu).  Launch with cudaGraphLaunch(exec, stream).
 cudaGraphExec_t cached_graph(Workspace& ws, int key, void (*body)(Workspace&, cudaStream_t));
+
+// Per-context function setup (abi.cu).  A dynamic shared-memory limit above
+// 48 KB is an attribute of a function *in one context*: it has to be set on
+// every device a process drives and again after pf_device_reset re-creates
+// the context.  set_smem_attr caches by (function, device, context
+// generation), so calling it before every launch costs a map lookup.
+void set_smem_attr(const void* fn, int bytes);
+// SM count of the current device (cached per device).
+int device_sms();
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor on the current device, after
+// set_smem_attr(fn, smem); cached like set_smem_attr.
+int occupancy(const void* fn, int threads, size_t smem);
+void note_context_reset(int device);  // pf_device_reset: invalidates the caches above
 
 // Registration: each k_*.cu module registers its descriptor at load time.
 void register_bench(int id, const BenchDesc* desc);
@@ -143,7 +156,7 @@ __global__ void init_kernel(float* out, int64_t n, F f) {
 template <class F>
 inline void launch_init_with(float* out, int64_t n, F f, cudaStream_t s) {
   int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > 148 * 32) blocks = 148 * 32;  // grid-stride: any device, 32 CTAs per B200 SM
   if (blocks < 1) blocks = 1;
   init_kernel<<<(unsigned)blocks, 256, 0, s>>>(out, n, f);
 }

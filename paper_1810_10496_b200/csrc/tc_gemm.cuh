@@ -417,7 +417,7 @@ inline int tc_splits(int64_t m, int64_t n, int64_t ktot) {
   const int64_t tiles = ((m + kTcBM - 1) / kTcBM) * ((n + bn - 1) / bn);
   const int64_t kblocks = (ktot + kTcBK - 1) / kTcBK;
   if (tiles >= 74) return 1;
-  int64_t s = std::min<int64_t>(148 / tiles, kblocks / 2);
+  int64_t s = std::min<int64_t>(device_sms() / tiles, kblocks / 2);
   return (int)std::max<int64_t>(1, s);
 }
 
@@ -465,12 +465,7 @@ __global__ void __launch_bounds__(256) tc_prescale_flat(float4* __restrict__ D, 
 
 template <BenchId Bn, int V, int BN>
 inline void launch_tc_main(const TcParams& p, int np, int mp, int zs, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tc_gemm_kernel<Bn, V, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TcCfg<BN>::kSmem);
-    configured = true;
-  }
+  set_smem_attr((const void*)tc_gemm_kernel<Bn, V, BN>, (int)TcCfg<BN>::kSmem);
   tc_gemm_kernel<Bn, V, BN><<<dim3(np / BN, mp / kTcBM, zs), 128, TcCfg<BN>::kSmem, s>>>(p);
 }
 

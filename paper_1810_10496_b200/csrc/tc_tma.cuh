@@ -705,7 +705,7 @@ inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair, bool uppe
     return e ? std::max(1, std::atoi(e)) : 1 << 30;
   }();
   int splits = 1;
-  if (ctas < 74) splits = (int)std::max<int64_t>(1, std::min<int64_t>(148 / ctas, kblocks / 2));
+  if (2 * ctas < device_sms()) splits = (int)std::max<int64_t>(1, std::min<int64_t>(device_sms() / ctas, kblocks / 2));
   splits = std::min(splits, cap);
   const int per = (kblocks + splits - 1) / splits;
   return (kblocks + per - 1) / per;
@@ -789,7 +789,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
       cudaMemset2DAsync(a.D, (size_t)a.ldd * sizeof(float), 0, (size_t)a.N * sizeof(float), a.M, s);
     else if (a.ldd == a.N && a.ldc == a.N && a.N % 4 == 0 && reinterpret_cast<uintptr_t>(a.D) % 16 == 0 &&
              reinterpret_cast<uintptr_t>(a.Cin) % 16 == 0)
-      tc_prescale_flat<Bn, V><<<4 * 148, 256, 0, s>>>(reinterpret_cast<float4*>(a.D),
+      tc_prescale_flat<Bn, V><<<4 * device_sms(), 256, 0, s>>>(reinterpret_cast<float4*>(a.D),
                                                        reinterpret_cast<const float4*>(a.Cin),
                                                        (int64_t)a.M * a.N / 4, a.beta);
     else
@@ -807,12 +807,8 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   p.D = a.D;
   p.ldd = a.ldd;
   p.upper_only = a.upper_only || p.sym;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tc_tma_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    cudaFuncSetAttribute(tc_tma2_kernel<Bn, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    configured = true;
-  }
+  set_smem_attr((const void*)tc_tma_kernel<Bn, V>, (int)kTmaSmem);
+  set_smem_attr((const void*)tc_tma2_kernel<Bn, V>, (int)kTmaSmem);
   {
     // after a beta pre-pass the GEMM is a programmatic dependent launch: its
     // prologue and mainloop overlap the pre-pass (griddepcontrol.wait gates
@@ -914,7 +910,7 @@ inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual,
 template <BenchId Bn, int V>
 inline bool launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t s) {
   TcGemmArgs a = a0;
-  a.tile_flags = ws.ensure_tile_flags();
+  a.tile_flags = ws.ensure_tile_flags(s);
   a.epoch = ++ws.tile_epoch;
   bool dlo = false;
   // symmetric products split-K their upper tiles but still profit from the
@@ -944,7 +940,7 @@ inline bool launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t
         if (!ops[i] || given[i] || done[i]) continue;
         for (int j = i; j < 4; ++j)
           if (!given[j] && ops[j] == ops[i] && off[j] == off[i]) done[j] = true;
-        tc_split_lo<Bn, V><<<4 * 148, 256, 0, s>>>(ops[i], lo + off[i], e[i]);
+        tc_split_lo<Bn, V><<<4 * device_sms(), 256, 0, s>>>(ops[i], lo + off[i], e[i]);
       }
       TcGemmArgs b = a;
       for (int i = 0; i < 4; ++i) {

@@ -88,10 +88,47 @@ class Dist:
             out.append(value)
         return out
 
+    def map_owned(self, fn, items: list, owners: list[int]) -> list:
+        """``[fn(x) for x in items]`` with item i evaluated on rank
+        ``owners[i]`` (device affinity), gathered to every rank in item
+        order; exceptions are re-raised on every rank as in ``map``."""
+        if not self.pg:
+            return [fn(x) for x in items]
+        local = {}
+        for i, x in enumerate(items):
+            if owners[i] != self.rank:
+                continue
+            try:
+                local[i] = (True, fn(x))
+            except Exception as exc:  # noqa: BLE001 -- re-raised below on every rank
+                local[i] = (False, exc)
+        merged: dict = {}
+        for part in self.gather(local):
+            merged.update(part)
+        out = []
+        for i in range(len(items)):
+            ok, value = merged[i]
+            if not ok:
+                raise value
+            out.append(value)
+        return out
+
     def close(self) -> None:
         if self.pg:
             self.pg.destroy_process_group()
             self.pg = None
+
+
+def assign(costs: list[float], world: int) -> list[int]:
+    """Owner rank of each item: longest-processing-time-first (ties by index)."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    loads = [0.0] * world
+    owner = [0] * len(costs)
+    for i in order:
+        r = min(range(world), key=lambda k: loads[k])
+        owner[i] = r
+        loads[r] += costs[i]
+    return owner
 
 
 def shard(work: list, costs: list[float], world: int, rank: int) -> list:

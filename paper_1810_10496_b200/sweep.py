@@ -12,6 +12,9 @@ runner process (toolchain.py:216-273).  Here:
 * ``evaluate_round`` runs a list of (workspace, variant) evaluations as one
   device batch (``pf_eval_batch``): back-to-back on one stream, one CUDA event
   pair per candidate, no host synchronisation in between;
+* ``explore_suite`` runs ``explore`` for several kernels with their device
+  work batched ahead (``B200Backend.prefetch_many``) -- the product path the
+  bench times;
 * ``shard`` splits work across GPUs for the one-process-per-GPU scheduler
   (independent evaluations, no collective; longest-processing-
   time-first by estimated cost).
@@ -27,7 +30,7 @@ from . import _abi, passmodel, registry
 from .backend.b200 import B200Backend, Workspace, family, variant_launches
 from .catalog import PassCatalog, PhaseOrder
 from .dist import shard
-from .explorer import ExplorationConfig, draw_orders
+from .explorer import ExplorationConfig, draw_orders, explore
 
 
 @dataclass(frozen=True)
@@ -87,6 +90,7 @@ def evaluate_round(items: list[tuple[Workspace, int]], restore: bool = True, flu
         if host_in is not None and id(ws) not in uploaded and ws in host_in:
             hin = _ptr_table(ws, host_in[ws])
             uploaded.add(id(ws))
+            ws.input_tag = None  # device inputs (and the pristine copy) are now the uploaded data
         hout = _ptr_table(ws, host_out[ws]) if host_out is not None and ws in host_out else None
         keep += [hin, hout]
         evals[i].host_in = ctypes.cast(hin, c_void_p) if hin is not None else None
@@ -97,8 +101,21 @@ def evaluate_round(items: list[tuple[Workspace, int]], restore: bool = True, flu
     return list(ms_each), total.value
 
 
+def explore_suite(kernels, catalog: PassCatalog, configs, backend: B200Backend, host_inputs: dict | None = None):
+    """The exploration step of ``cmd_explore`` (cli.py:168-218) for several
+    kernels: ``explorer.explore`` per kernel, unchanged, with the device work
+    of every kernel's fresh evaluations batched ahead of it
+    (``B200Backend.prefetch_many``: one batch per kernel, issued by the
+    device worker while the engine walks the previous kernel's records).
+    Returns {kernel id: sorted records}, the same records ``explore`` gives
+    without prefetching."""
+    jobs = [(k, draw_orders(catalog, c)) for k, c in zip(kernels, configs)]
+    backend.prefetch_many(jobs, host_inputs)
+    return {k.id: explore(k, catalog, c, backend) for k, c in zip(kernels, configs)}
+
+
 def launches_of(items: list[tuple[Workspace, int]]) -> int:
     return sum(variant_launches(ws.bench, v, ws.dims) for ws, v in items)
 
 
-__all__ = ["Candidate", "candidate_set", "evaluate_round", "launches_of", "shard"]
+__all__ = ["Candidate", "candidate_set", "evaluate_round", "explore_suite", "launches_of", "shard"]

@@ -42,6 +42,35 @@ def phaseforge():
     return phaseforge
 
 
+BASELINE_REF = ROOT / "baseline" / "_ref"
+
+
+def reference_engine_path() -> Path | None:
+    """Where the unmodified reference package can be imported from: the
+    read-only source tree (this container) or its pip install under
+    baseline/_ref (git-ignored, travels to the GPU box with the snapshot)."""
+    if have_reference():
+        return REFERENCE_SRC
+    if (BASELINE_REF / "phaseforge" / "__init__.py").exists():
+        return BASELINE_REF
+    return None
+
+
+@pytest.fixture(scope="session")
+def reference_engine():
+    """The unmodified reference ``phaseforge`` package (test oracle and
+    drop-in driver; never imported by the product)."""
+    path = reference_engine_path()
+    if path is None:
+        pytest.skip("reference package not available (neither /root/reference nor baseline/_ref)")
+    sys.dont_write_bytecode = True
+    if str(path) not in sys.path:
+        sys.path.append(str(path))
+    import phaseforge  # noqa: WPS433
+
+    return phaseforge
+
+
 @pytest.fixture(scope="session")
 def gpu_backend():
     from paper_1810_10496_b200.backend.b200 import B200Backend, device_count

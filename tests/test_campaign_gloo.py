@@ -1,8 +1,8 @@
 """The rank-parallel campaign on world_size 2 (gloo,
-CPU): with a deterministic backend, sharding explore's fresh evaluations,
-finalize's candidates, reduce_order's speculative deletion windows, the
-measurement reps and the LOO kernels over two ranks gives exactly the
-single-process result -- the same KB, records, report and LOO curves on both
+CPU): kernels are sharded over the ranks with device affinity (every timed
+run of a kernel on its owner's device: explore, finalize, reduce_order and
+its LOO curves); with a deterministic backend the result is exactly the
+single-process one -- the same KB, records, report and LOO curves on both
 ranks."""
 
 from __future__ import annotations
@@ -101,17 +101,12 @@ def _worker(rank, world, port, q):
         d.close()
 
 
-def test_parallel_helpers_equal_explorer_serially():
-    be, k = HashBackend(), _kernels()[0]
-    cat = campaign.passmodel.default_catalog()
-    ser = lambda f, xs, costs=None: [f(x) for x in xs]  # noqa: E731
-    assert campaign.explore_parallel(k, cat, CFG, be, ser) == explorer.explore(k, cat, CFG, be)
-    recs = explorer.explore(k, cat, CFG, be)
-    best = explorer.finalize(k, recs, CFG, be)
-    assert campaign.finalize_parallel(k, recs, CFG, be, ser) == best
-    for width in (1, 2, 3, 5):
-        assert (campaign.reduce_order_parallel(k, best[0], be, 0.01, CFG, ser, width)
-                == explorer.reduce_order(k, best[0], be, 0.01, CFG))
+def test_kernel_owners_lpt_and_affinity():
+    ks = _kernels()
+    assert campaign.kernel_owners(ks, 1) == [0, 0, 0, 0]
+    owners = campaign.kernel_owners(ks, 2, {"GEMM": 10.0, "ATAX": 1.0, "2DCONV": 1.0, "SYRK": 8.0})
+    assert owners[0] != owners[3]  # the two expensive kernels go to different ranks
+    assert sorted(set(owners)) == [0, 1]
 
 
 @pytest.mark.timeout(300)

@@ -183,7 +183,11 @@ def test_tensor_core_config_paths_match_oracle(bench, gpu_backend):
 
 # Stencil tiling edges: partial 128-wide k tiles, j tiles and i runs that end
 # mid-tile, tiny volumes where a run spans several column tiles.
-STENCIL_SIZES = {"3DCONV": [(37, 45, 132), (9, 20, 8), (64, 33, 260)], "2DCONV": [(67, 516), (5, 8)]}
+# FDTD-2D: the register-tiled temporal blocking (stage 2) needs ny % 4 == 0 and
+# only spans several column tiles when ny > 112; enough steps that region-edge
+# errors would reach the stored columns and rows (halo width).
+STENCIL_SIZES = {"3DCONV": [(37, 45, 132), (9, 20, 8), (64, 33, 260)], "2DCONV": [(67, 516), (5, 8)],
+                 "FDTD-2D": [(64, 256, 12), (128, 512, 30), (40, 1000, 13), (150, 236, 9)]}
 
 
 @pytest.mark.parametrize("bench", [b for b in STENCIL_SIZES if b in BUILT])

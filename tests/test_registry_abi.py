@@ -38,7 +38,7 @@ def test_library_loads_and_exports_header_symbols():
     assert len(names) >= 25
     for n in names:
         assert hasattr(lib, n), f"libpfgpu.so does not export {n}"
-    assert lib.pf_abi_version() == 1
+    assert lib.pf_abi_version() == 2
     assert lib.pf_bench_count() == 15
 
 
