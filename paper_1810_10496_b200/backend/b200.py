@@ -40,6 +40,7 @@ import contextlib
 import ctypes
 import gzip
 import json
+import operator
 import statistics
 import sys
 from collections import OrderedDict
@@ -52,6 +53,7 @@ from . import types as _own_types
 from .types import Artifact, Backend, BackendError, KernelCase
 
 ARTIFACTS_PATH = Path(__file__).resolve().parent.parent / "artifacts.json.gz"
+_NAME = operator.attrgetter("name")
 ARTIFACT_MAGIC = "pfgpu-artifact/1"
 
 
@@ -345,7 +347,7 @@ class B200Backend(Backend):
 
     def variant_for(self, kernel: KernelCase, order) -> tuple[str, int]:
         bench = registry.bench_of(kernel)
-        key = (bench, tuple(p.name for p in order.passes))
+        key = (bench, tuple(map(_NAME, order.passes)))
         v = self._variant_memo.get(key)
         if v is None:
             if not isinstance(order, PhaseOrder):  # a foreign (reference) PhaseOrder: same pass names
@@ -610,9 +612,27 @@ class B200Backend(Backend):
         return total
 
     def _submit_job(self, kernel: KernelCase, orders) -> int:
-        cands = self.fresh_candidates(kernel, orders)
-        if not cands:
-            return 0
+        """Walk ``orders`` (any iterable, e.g. a lazy draw) in geometrically
+        growing chunks and submit each chunk's new fresh candidates as one
+        batch: the device starts on the first candidates while the host is
+        still compiling the rest of the stream."""
+        seen, total, chunk, pending = set(), 0, 16, []
+        for i, order in enumerate(orders):
+            c = self.compile(kernel, order)
+            if c.is_ok and c.artifact.digest not in seen:
+                seen.add(c.artifact.digest)
+                bench, variant = self.variant_for(kernel, order)
+                pending.append((bench, variant, c.artifact.digest))
+            if i + 1 == chunk:
+                if pending:
+                    total += self._submit_cands(kernel, pending)
+                    pending = []
+                chunk *= 4
+        if pending:
+            total += self._submit_cands(kernel, pending)
+        return total
+
+    def _submit_cands(self, kernel: KernelCase, cands) -> int:
         _, vdims = registry.parse_descriptor(kernel.validation_input)
         _, mdims = registry.parse_descriptor(kernel.measurement_input)
         plan = [(bench, variant, digest, self.workspace(bench, vdims, True, -1),

@@ -8,14 +8,19 @@
 //          the paper's 5.4x CORR case).
 // stage 1  row-split column statistics (atomics) and the Gram matrix D^T D
 //          as an upper-triangle tiled SIMT GEMM + mirror.
-// stage 2  the normalisation pass also writes the centred (scaled) data
-//          transposed into an aligned m x n scratch (64x64 shared-memory
-//          tiles), with its 3xTF32 lo image, so the Gram matrix X X^T runs
-//          pre-split on the TMA-fed tcgen05
-//          3xTF32 kernel exactly like SYRK (upper-triangle tiles, K-major
-//          operands, TMA epilogue into an aligned m x m scratch); one tiled
-//          pass then scatters it into the 1-based symmat with the mirror (and
-//          CORR's unit diagonal) folded in.
+// stage 2  four launches: (1) one pass over data accumulates every column's
+//          sum and sum of squares in fp64 (row splits, fp64 atomics) and the
+//          last block of each column finishes mean (and CORR's std) --
+//          sum (x - mu)^2 = S2 - 2 mu S1 + n mu^2 exactly in fp64; (2) the
+//          centred (scaled) data and its 3xTF32 lo image are written into an
+//          aligned scratch (the data itself is not
+//          written back: it is not in the compare set, and its pristine copy
+//          is restored before every run anyway), transposed into a K-major
+//          operand; (3) the Gram matrix on the TMA-fed tcgen05 3xTF32 kernel
+//          with pre-split operands (upper-triangle pair tiles, 2-way split-K
+//          with the ordered hand-over) into an aligned m x m scratch; (4) one
+//          tiled pass scatters it into the 1-based symmat with the mirror
+//          (and CORR's unit diagonal) folded in.
 #pragma once
 #include "pf_common.cuh"
 #include "simt_gemm.cuh"
@@ -173,14 +178,63 @@ inline void launch_colstat(const float* data, const float* mean, float* out, int
   finalize_stat<Bn, V, kPass><<<cdiv(m, 256), 256, 0, s>>>(out, m);
 }
 
-// Stage 2: normalise in place (reduce_s0's arithmetic) and write the result
-// transposed: xt[(j-1) * ldx + i-1] = data[i][j].  Block (32, 8) on a 64x64
-// tile: 16 elements per thread, all loads issued before the first store.
+// 64x64 tiles of the symmat scatter (stage-2 fallback)
 constexpr int kCT = 64;
 
+// ---- stage 2: fused column statistics.  acc[0..m] = S1, acc[m+1..2m+1] = S2
+// (fp64, zeroed before the launch), blockIdx.y = row split; the last block of
+// a column split group (a per-column-block arrival counter) finishes the
+// statistics for its 256 columns.
 template <BenchId Bn, int V, bool kCorr>
-__global__ void __launch_bounds__(256) reduce_transpose(const float* __restrict__ mean, const float* __restrict__ stdv,
-                                                        float* data, float* __restrict__ xt,
+__global__ void __launch_bounds__(256) colstats_fused(const float* __restrict__ data, double* acc, unsigned* arrivals,
+                                                      float* mean, float* stdv, int m, int n, int rps) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  const int i0 = 1 + blockIdx.y * rps;
+  const int i1 = min(n + 1, i0 + rps);
+  if (j <= m) {
+    double s1 = 0.0, s2 = 0.0;
+    int i = i0;
+    for (; i + 3 < i1; i += 4) {  // four loads in flight per thread
+      const float a = __ldg(data + (size_t)i * (m + 1) + j), b = __ldg(data + (size_t)(i + 1) * (m + 1) + j);
+      const float c = __ldg(data + (size_t)(i + 2) * (m + 1) + j), d = __ldg(data + (size_t)(i + 3) * (m + 1) + j);
+      s1 += ((double)a + b) + ((double)c + d);
+      if constexpr (kCorr) s2 += ((double)a * a + (double)b * b) + ((double)c * c + (double)d * d);
+    }
+    for (; i < i1; ++i) {
+      const float a = __ldg(data + (size_t)i * (m + 1) + j);
+      s1 += a;
+      if constexpr (kCorr) s2 += (double)a * a;
+    }
+    atomicAdd(acc + j, s1);
+    if constexpr (kCorr) atomicAdd(acc + (m + 1) + j, s2);
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(arrivals + blockIdx.x, 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last || j > m) return;
+  __threadfence();
+  const double S1 = atomicAdd(acc + j, 0.0);  // coherent read of the completed sums
+  const float mu = (float)(S1 / (double)kFloatN);
+  mean[j] = mu;
+  if constexpr (kCorr) {
+    const double S2 = atomicAdd(acc + (m + 1) + j, 0.0);
+    const double q = S2 - 2.0 * (double)mu * S1 + (double)n * (double)mu * (double)mu;
+    const float sd = (float)sqrt(fmax(q, 0.0) / (double)kFloatN);
+    stdv[j] = sd <= kEps ? 1.0f : sd;
+  }
+}
+
+// Xt[j-1][i-1] = centred (CORR: scaled) data[i][j] -- the data transposed
+// into a K-major m x n operand (pitch ldx, a multiple of 4) -- and its 3xTF32
+// lo image.  Block (32, 8) on a 64x64 tile through shared memory: 16
+// elements per thread, all loads issued before the first store.  (Writing X
+// untransposed and running the Gram with MN-major operands measured slower:
+// 68 vs 54 us for the 2048^2 Gram.)
+template <BenchId Bn, int V, bool kCorr>
+__global__ void __launch_bounds__(256) centre_transpose(const float* __restrict__ data, const float* __restrict__ mean,
+                                                        const float* __restrict__ stdv, float* __restrict__ xt,
                                                         float* __restrict__ xt_lo, int m, int n, int ldx) {
   __shared__ float t[kCT][kCT + 1];
   const int j0 = blockIdx.x * kCT, i0 = blockIdx.y * kCT;
@@ -197,19 +251,15 @@ __global__ void __launch_bounds__(256) reduce_transpose(const float* __restrict_
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int i = i0 + threadIdx.y + 8 * q + 1, j = j0 + threadIdx.x + 32 * c + 1;
-      v[q][c] = (i <= n && j <= m) ? data[(size_t)i * (m + 1) + j] : 0.f;
+      v[q][c] = (i <= n && j <= m) ? __ldg(data + (size_t)i * (m + 1) + j) : 0.f;
     }
 #pragma unroll
   for (int q = 0; q < kCT / 8; ++q)
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const int r = threadIdx.y + 8 * q, i = i0 + r + 1, j = j0 + threadIdx.x + 32 * c + 1;
-      if (i <= n && j <= m) {
-        float x = v[q][c] - mu[c];
-        if constexpr (kCorr) x /= sc[c];
-        data[(size_t)i * (m + 1) + j] = x;
-        t[r][threadIdx.x + 32 * c] = x;
-      }
+      float x = v[q][c] - mu[c];
+      if constexpr (kCorr) x /= sc[c];
+      t[threadIdx.y + 8 * q][threadIdx.x + 32 * c] = x;
     }
   __syncthreads();
 #pragma unroll
@@ -220,7 +270,7 @@ __global__ void __launch_bounds__(256) reduce_transpose(const float* __restrict_
       if (j < m && i < n) {
         const float x = t[threadIdx.x + 32 * c][threadIdx.y + 8 * q];
         xt[(size_t)j * ldx + i] = x;
-        xt_lo[(size_t)j * ldx + i] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);  // 3xTF32 lo image
+        xt_lo[(size_t)j * ldx + i] = x - tma::trunc_tf32(x);
       }
     }
 }
@@ -275,34 +325,51 @@ inline void run(Workspace& ws, cudaStream_t s) {
     reduce_s0<Bn, V, kCorr><<<dim3(cdiv(m, kBX), cdiv(n, kBY)), dim3(kBX, kBY), 0, s>>>(mean, stdv, data, m, n);
     gram_s0<Bn, V, kStore, kUnroll, kLsr, kCorr><<<cdiv(m, kB1), kB1, 0, s>>>(sym, data, m, n);
   } else {
-    launch_colstat<Bn, V, 0>(data, nullptr, mean, m, n, s);
-    if constexpr (kCorr) launch_colstat<Bn, V, 1>(data, mean, stdv, m, n, s);
     if constexpr (kStage == 2) {
-      // 16-byte pitches for the TMA maps (K tail beyond n reads as zero)
-      const int np = (n + 3) / 4 * 4, mp = (m + 3) / 4 * 4;
-      float* xt = ws.ensure_scratch((2 * (size_t)m * np + (size_t)m * mp) * sizeof(float));
-      if (!xt) {
+      // scratch: Xt and Xt_lo (m x np: the K-major Gram operand; 16-byte
+      // pitch for the TMA maps, the K tail reads as zero), G (m x mp: split
+      // 0's partial sums, or the whole Gram for the scatter fallback), then
+      // the fp64 column sums and the per-column-block arrival counters
+      const int mp = (m + 3) / 4 * 4, np = (n + 3) / 4 * 4;
+      const size_t xs = (size_t)m * np, gs = (size_t)m * mp;
+      const int gx = (int)cdiv(m, 256);
+      float* X = ws.ensure_scratch((2 * xs + gs) * sizeof(float) + 2 * (m + 1) * sizeof(double) + 64 * 4 +
+                                   gx * sizeof(unsigned));
+      if (!X) {
         launch_failed("CORR/COVAR stage 2: scratch allocation failed");
         return;
       }
-      float* xt_lo = xt + (size_t)m * np;
-      float* G = xt_lo + (size_t)m * np;
-      reduce_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(mean, stdv, data, xt,
-                                                                                           xt_lo, m, n, np);
-      // the transpose also writes the lo image, so the Gram runs pre-split
-      // (no converter warps) at no extra pass
-      TcGemmArgs g{m, m, n, 1.f, 0.f, xt, np, false, xt, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
-      g.Alo = xt_lo;
-      g.Blo = xt_lo;
+      float* Xlo = X + xs;
+      float* G = Xlo + xs;
+      double* acc = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(G + gs) + 255) & ~uintptr_t(255));
+      unsigned* arrivals = reinterpret_cast<unsigned*>(acc + 2 * (m + 1));
+      cudaMemsetAsync(acc, 0, 2 * (m + 1) * sizeof(double) + gx * sizeof(unsigned), s);
+      int splits = std::max(1, std::min((int)cdiv(device_sms() * 4, gx), (n + 31) / 32));
+      const int rps = (int)cdiv(n, splits);
+      splits = (int)cdiv(n, rps);
+      colstats_fused<Bn, V, kCorr><<<dim3(gx, splits), 256, 0, s>>>(data, acc, arrivals, mean, stdv, m, n, rps);
+      centre_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(data, mean, stdv, X,
+                                                                                            Xlo, m, n, np);
+      // Xt Xt^T with K-major operands
+      TcGemmArgs g{m, m, n, 1.f, 0.f, X, np, false, X, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
+      g.Alo = Xlo;
+      g.Blo = Xlo;
       g.tile_flags = ws.ensure_tile_flags(s);
       g.epoch = ++ws.tile_epoch;
       if (!launch_tc_tma<Bn, V>(g, s)) {
         launch_failed("CORR/COVAR stage 2: TMA operand maps rejected");
         return;
       }
+      // (Writing symmat from the Gram epilogue instead -- plain stores of
+      // each tile and its mirror, 256x128 pair tiles without split-K -- was
+      // measured slower on B200: 68.7 us vs 47.1 us Gram + 8.5 us scatter;
+      // the unaligned 1-based rows turn the epilogue's stores into partial
+      // sector writes.)
       sym_scatter<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(m, kCT)), dim3(32, 8), 0, s>>>(G, mp, sym, m);
       return;
     }
+    launch_colstat<Bn, V, 0>(data, nullptr, mean, m, n, s);
+    if constexpr (kCorr) launch_colstat<Bn, V, 1>(data, mean, stdv, m, n, s);
     reduce_s0<Bn, V, kCorr><<<dim3(cdiv(m, kBX), cdiv(n, kBY)), dim3(kBX, kBY), 0, s>>>(mean, stdv, data, m, n);
     const float* d1 = data + (m + 1) + 1;  // data[1][1]
     float* s1 = sym + (m + 1) + 1;         // symmat[1][1]
@@ -316,7 +383,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
 inline int64_t launches(bool corr, int stage, int64_t m, int64_t n) {
   if (stage == 0) return corr ? 4 : 3;
   const int64_t stats = corr ? 4 : 2;
-  if (stage == 2) return stats + 1 + tc_tma_launches(m, m, n, false, true, true) + 1;
+  if (stage == 2) return 2 + tc_tma_launches(m, m, n, false, true, true) + 1;  // stats, centre, Gram, scatter
   return stats + 1 + 1 + 1 + (corr ? 1 : 0);
 }
 

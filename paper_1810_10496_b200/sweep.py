@@ -25,10 +25,11 @@ from __future__ import annotations
 import ctypes
 from ctypes import byref, c_float, c_void_p
 from dataclasses import dataclass
+from random import Random
 
 from . import _abi, passmodel, registry
 from .backend.b200 import B200Backend, Workspace, family, variant_launches
-from .catalog import PassCatalog, PhaseOrder
+from .catalog import PassCatalog, PhaseOrder, random_phase_order
 from .dist import shard
 from .explorer import ExplorationConfig, draw_orders, explore
 
@@ -101,6 +102,14 @@ def evaluate_round(items: list[tuple[Workspace, int]], restore: bool = True, flu
     return list(ms_each), total.value
 
 
+def _lazy_orders(catalog: PassCatalog, config: ExplorationConfig):
+    """``draw_orders(catalog, config)`` one order at a time (same RNG use,
+    explorer.py:163-167), so batches can start before the stream is drawn."""
+    rng = Random(config.seed)
+    for _ in range(config.num_sequences):
+        yield random_phase_order(catalog, config.max_len, rng)
+
+
 def explore_suite(kernels, catalog: PassCatalog, configs, backend: B200Backend, host_inputs: dict | None = None):
     """The exploration step of ``cmd_explore`` (cli.py:168-218) for several
     kernels: ``explorer.explore`` per kernel, unchanged, with the device work
@@ -109,7 +118,7 @@ def explore_suite(kernels, catalog: PassCatalog, configs, backend: B200Backend, 
     device worker while the engine walks the previous kernel's records).
     Returns {kernel id: sorted records}, the same records ``explore`` gives
     without prefetching."""
-    jobs = [(k, draw_orders(catalog, c)) for k, c in zip(kernels, configs)]
+    jobs = [(k, _lazy_orders(catalog, c)) for k, c in zip(kernels, configs)]
     backend.prefetch_many(jobs, host_inputs)
     return {k.id: explore(k, catalog, c, backend) for k, c in zip(kernels, configs)}
 

@@ -82,7 +82,7 @@ def test_sharded_campaign_on_gpu():
         mine = [k.id for k, o in zip(kernels, owners) if o == rank]
         assert [m for m in got[rank][1] if m in BENCHES] == mine
     kb, records, geo, loo, variants = got[0][0]
-    assert set(kb) == set(serial[0]) == set(BENCHES)
+    assert set(kb["entries"]) == set(serial[0]["entries"]) == set(BENCHES)
     assert {r[0] for r in records} == set(BENCHES) and len(records) == len(serial[1])
     assert geo > 1.0 and set(loo) == set(serial[3])
     assert variants["GEMM"] == serial[4]["GEMM"]  # the tcgen05 variant wins on either layout

@@ -48,7 +48,7 @@ def test_prefetched_explore_matches_sequential(gpu_backend):
     seq.close()
     be = B200Backend(device=0, samples=1)
     got = explore_suite(cases, cat, cfgs, be)
-    assert be.prefetch_batches == len(cases)
+    assert be.prefetch_batches >= len(cases)  # chunked: at least one batch per kernel
     runs_after_batches = be.device_runs
     for c in cases:
         assert _strip(sorted(got[c.id], key=lambda r: r.eval_index)) == \
