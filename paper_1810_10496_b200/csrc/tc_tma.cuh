@@ -137,6 +137,27 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
                : "memory");
 }
 
+// Converter warps (128 threads, t = 0..127): lo = x - trunc_tf32(x) for
+// COUNT float4 per thread of a stage (raw at `raw`, lo image at `lo`), eight
+// shared-memory loads in flight before their stores (the lds/sts asm
+// statements are volatile, so a load-store-load order would serialise them).
+template <int COUNT>
+__device__ __forceinline__ void split_lo(uint32_t raw, uint32_t lo, int t) {
+#pragma unroll
+  for (int b = 0; b < COUNT; b += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b + u < COUNT) v[u] = lds128(raw + 16u * (uint32_t)(t + 128 * (b + u)));
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b + u < COUNT)
+        sts128(lo + 16u * (uint32_t)(t + 128 * (b + u)),
+               make_float4(v[u].x - trunc_tf32(v[u].x), v[u].y - trunc_tf32(v[u].y), v[u].z - trunc_tf32(v[u].z),
+                           v[u].w - trunc_tf32(v[u].w)));
+  }
+}
+
 __device__ __forceinline__ void store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -380,12 +401,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       tc::mbar_wait(tc::smem_u32(&full_bar[s]), ph);
       const uint32_t raw = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
       const uint32_t lo = raw + 2 * kTmaTileBytes;
-#pragma unroll 4
-      for (int q = ct; q < ((p.diag & 1) || p.presplit ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
-        const float4 v = tma::lds128(raw + 16u * q);
-        tma::sts128(lo + 16u * q, make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
-                                              v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w)));
-      }
+      if (!((p.diag & 1) || p.presplit)) tma::split_lo<(int)(2 * kTmaTileBytes / 16 / 128)>(raw, lo, ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(tc::smem_u32(&ready_bar[s]));
@@ -599,12 +615,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       tc2::wait(tc::smem_u32(&full_bar[s]), ph);
       const uint32_t raw = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
       const uint32_t lo = raw + 2 * kTmaTileBytes;
-#pragma unroll 4
-      for (int q = ct; q < ((p.diag & 1) || p.presplit ? 0 : (int)(2 * kTmaTileBytes / 16)); q += 128) {
-        const float4 v = tma::lds128(raw + 16u * q);
-        tma::sts128(lo + 16u * q, make_float4(v.x - tma::trunc_tf32(v.x), v.y - tma::trunc_tf32(v.y),
-                                              v.z - tma::trunc_tf32(v.z), v.w - tma::trunc_tf32(v.w)));
-      }
+      if (!((p.diag & 1) || p.presplit)) tma::split_lo<(int)(2 * kTmaTileBytes / 16 / 128)>(raw, lo, ct);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) tc2::arrive_remote(tc2::peer_addr(tc::smem_u32(&ready_bar[s]), 0));
@@ -707,6 +718,12 @@ inline TmaProbe& tma_probe() {
   return p;
 }
 
+}  // namespace pf
+
+#include "tc_splitk.cuh"  // small products: split-K in a cluster (needs the map helpers above)
+
+namespace pf {
+
 // CTA-pair (256x256) tiles for products with at least one full pair tile;
 // PF_TC_PAIR=0 in the environment forces the single-CTA kernel (A/B runs).
 inline bool tc_pair_ok(int64_t m, int64_t n) {
@@ -741,6 +758,8 @@ inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair, bool uppe
 template <BenchId Bn, int V>
 inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written = nullptr) {
   if (dlo_written) *dlo_written = false;
+  // small single products: split-K inside a cluster, DSMEM reduction (one launch)
+  if (!a.sym && !a.upper_only && !a.A2 && launch_tc_splitk<Bn, V>(a, s)) return true;
   TmaParams p;
   std::memset(&p, 0, sizeof(p));
   p.mn_lbo = tma_probe().lbo;
@@ -861,6 +880,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
 // launches of one TMA-path product: [prescale] + gemm
 inline int64_t tc_tma_launches(int64_t m, int64_t n, int64_t k, bool dual = false, bool upper = false,
                                bool beta_zero = false) {
+  if (tc_splitk_factor(m, n, k, dual, upper)) return 1;  // cluster split-K kernel
   const int kblocks = (int)((dual ? 2 : 1) * ((k + 31) / 32));
   const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, upper) <= 2;
   const bool split = tc_tma_splits(m, n, kblocks, pair, upper) > 1;
