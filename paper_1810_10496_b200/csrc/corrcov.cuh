@@ -275,6 +275,178 @@ __global__ void __launch_bounds__(256) centre_transpose(const float* __restrict_
     }
 }
 
+// ---- stage 2, fused: column statistics + centre/scale + transpose + lo
+// split in ONE cooperative launch (replaces colstats_fused + centre_transpose:
+// the data is read from HBM once and never re-read).  The data is cut into
+// 128 x 128 tiles; each CTA (one per SM) loads up to kStatTiles of them into
+// shared memory while accumulating per-thread fp64 column sums, writes its
+// per-tile column partials P[row tile][col] (no atomics, every slot written
+// exactly once), passes a grid barrier, sums the row-tile partials of its
+// columns in a fixed order (deterministic), and writes the centred (scaled)
+// tile transposed into Xt / Xt_lo straight from shared memory.  The float
+// arithmetic of mean / std / x' is exactly colstats_fused + centre_transpose's.
+constexpr int kStatTile = 128, kStatTiles = 2, kStatThreads = 256;
+constexpr int kStatPitch = kStatTile + 1;  // conflict-free column reads
+constexpr size_t kStatSmem = (size_t)kStatTiles * kStatTile * kStatPitch * sizeof(float) + 2 * 2 * kStatTile * sizeof(double);
+
+// kF16: the Gram runs on 3xFP16 images (tc_f16.cuh) -- xt / xt_lo are fp16
+// hi / lo images of x' * s, s = scale_of(bound) written to scale[0], with
+// bound = 2 (CORR: |x'| <= 1 since sum_i x'^2 = 1, or <= 0.005 for clamped
+// columns) or 2 max|data| (COVAR: |x - mu| <= 2 max|x|); each tile's max|x|
+// goes to tmax[] in phase 1.  Else fp32 x' and its 3xTF32 lo image.
+template <BenchId Bn, int V, bool kCorr, bool kF16>
+__global__ void __launch_bounds__(kStatThreads, 1)
+    stats_centre_coop(const float* __restrict__ data, double* part, float* tmax, int* flags, int epoch, float* mean,
+                      float* stdv, void* __restrict__ xt_, void* __restrict__ xt_lo_, float* scale, int m, int n,
+                      int ldx) {
+  extern __shared__ float st_smem[];
+  __shared__ float bred[8];
+  double* red = reinterpret_cast<double*>(st_smem + kStatTiles * kStatTile * kStatPitch);  // [2][2][128]
+  const int ct = (m + kStatTile - 1) / kStatTile, rt = (n + kStatTile - 1) / kStatTile;
+  const int ntiles = ct * rt;
+  const int c = threadIdx.x & (kStatTile - 1), h = threadIdx.x >> 7;  // column, row parity
+  // ---- phase 1: loads (64 per thread per tile in flight) + column partials
+#pragma unroll 1
+  for (int q = 0; q < kStatTiles; ++q) {
+    const int tile = blockIdx.x + q * gridDim.x;
+    if (tile >= ntiles) break;
+    const int r0 = (tile / ct) * kStatTile, c0 = (tile % ct) * kStatTile;
+    float* t = st_smem + q * kStatTile * kStatPitch;
+    const int j = c0 + c + 1;
+    float v[kStatTile / 2];
+#pragma unroll
+    for (int e = 0; e < kStatTile / 2; ++e) {
+      const int i = r0 + h + 2 * e + 1;
+      v[e] = (i <= n && j <= m) ? __ldg(data + (size_t)i * (m + 1) + j) : 0.f;
+    }
+    double s1 = 0.0, s2 = 0.0;
+    float vmax = 0.f;
+#pragma unroll
+    for (int e = 0; e < kStatTile / 2; e += 4) {
+      s1 += ((double)v[e] + v[e + 1]) + ((double)v[e + 2] + v[e + 3]);
+      if constexpr (kCorr)
+        s2 += ((double)v[e] * v[e] + (double)v[e + 1] * v[e + 1]) + ((double)v[e + 2] * v[e + 2] + (double)v[e + 3] * v[e + 3]);
+      if constexpr (kF16 && !kCorr)
+        vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(v[e]), fabsf(v[e + 1])), fmaxf(fabsf(v[e + 2]), fabsf(v[e + 3]))));
+    }
+#pragma unroll
+    for (int e = 0; e < kStatTile / 2; ++e) t[(h + 2 * e) * kStatPitch + c] = v[e];
+    red[(h * 2 + 0) * kStatTile + c] = s1;
+    if constexpr (kCorr) red[(h * 2 + 1) * kStatTile + c] = s2;
+    if constexpr (kF16 && !kCorr) {
+      vmax = f16op::block_max(vmax, bred);
+      if (threadIdx.x == 0) tmax[tile] = vmax;
+    }
+    __syncthreads();
+    if (h == 0 && j <= m) {
+      const size_t slot = (size_t)(r0 / kStatTile) * m + (j - 1);
+      part[slot] = red[c] + red[2 * kStatTile + c];
+      if constexpr (kCorr) part[(size_t)rt * m + slot] = red[kStatTile + c] + red[3 * kStatTile + c];
+    }
+    __syncthreads();
+  }
+  grid_barrier(flags, epoch);
+  float sc16 = 1.f;  // fp16 image scale
+  if constexpr (kF16) {
+    float bound = 2.f;
+    if constexpr (!kCorr) {
+      float mx = 0.f;
+      for (int k = threadIdx.x; k < ntiles; k += kStatThreads) mx = fmaxf(mx, __ldcg(tmax + k));
+      mx = f16op::block_max(mx, bred);
+      if (threadIdx.x == 0) bred[0] = mx;
+      __syncthreads();
+      bound = 2.f * bred[0];
+      __syncthreads();
+    }
+    sc16 = f16op::scale_of(bound);
+    if (blockIdx.x == 0 && threadIdx.x == 0) scale[0] = sc16;
+  }
+  // ---- phase 2: statistics of this CTA's columns, then the transposed tiles
+#pragma unroll 1
+  for (int q = 0; q < kStatTiles; ++q) {
+    const int tile = blockIdx.x + q * gridDim.x;
+    if (tile >= ntiles) break;
+    const int r0 = (tile / ct) * kStatTile, c0 = (tile % ct) * kStatTile;
+    float* t = st_smem + q * kStatTile * kStatPitch;
+    float* mus = reinterpret_cast<float*>(red);  // [2][128] floats: mu, scale
+    if (threadIdx.x < kStatTile) {
+      const int j = c0 + threadIdx.x + 1;
+      float mu = 0.f, sc = 1.f;
+      if (j <= m) {
+        double S1 = 0.0, S2 = 0.0;
+        for (int r = 0; r < rt; ++r) {
+          S1 += __ldcg(part + (size_t)r * m + (j - 1));
+          if constexpr (kCorr) S2 += __ldcg(part + (size_t)(rt + r) * m + (j - 1));
+        }
+        mu = (float)(S1 / (double)kFloatN);
+        float sd = 1.f;
+        if constexpr (kCorr) {
+          const double qq = S2 - 2.0 * (double)mu * S1 + (double)n * (double)mu * (double)mu;
+          const float sdv = (float)sqrt(fmax(qq, 0.0) / (double)kFloatN);
+          sd = sdv <= kEps ? 1.0f : sdv;
+          sc = sqrtf(kFloatN) * sd;
+        }
+        if (r0 == 0) {
+          mean[j] = mu;
+          if constexpr (kCorr) stdv[j] = sd;
+        }
+      }
+      mus[threadIdx.x] = mu;
+      mus[kStatTile + threadIdx.x] = sc;
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if constexpr (kF16) {
+      // warp w: columns w, w + 8, ...; lane: rows 2 lane + 64 e, +1 (one half2 each: 128-byte rows)
+      __half* xh = reinterpret_cast<__half*>(xt_);
+      __half* xl = reinterpret_cast<__half*>(xt_lo_);
+#pragma unroll 2
+      for (int cc = w; cc < kStatTile; cc += kStatThreads / 32) {
+        const int j = c0 + cc;
+        if (j >= m) break;
+        const float mu = mus[cc], sc = mus[kStatTile + cc];
+#pragma unroll
+        for (int e = 0; e < kStatTile / 64; ++e) {
+          const int r = 2 * lane + 64 * e, i = r0 + r;
+          if (i < n) {
+            float x0 = t[r * kStatPitch + cc] - mu, x1 = t[(r + 1) * kStatPitch + cc] - mu;
+            if constexpr (kCorr) {
+              x0 /= sc;
+              x1 /= sc;
+            }
+            __half2 hh, ll;
+            f16op::split1(x0, sc16, hh.x, ll.x);
+            f16op::split1(i + 1 < n ? x1 : 0.f, sc16, hh.y, ll.y);
+            *reinterpret_cast<__half2*>(xh + (size_t)j * ldx + i) = hh;  // ldx, i even: 4-byte aligned
+            *reinterpret_cast<__half2*>(xl + (size_t)j * ldx + i) = ll;
+          }
+        }
+      }
+    } else {
+      float* xt = reinterpret_cast<float*>(xt_);
+      float* xt_lo = reinterpret_cast<float*>(xt_lo_);
+      // warp w: columns w, w + 8, ...; lane: rows lane + 32 e (128-byte rows of Xt)
+#pragma unroll 4
+      for (int cc = w; cc < kStatTile; cc += kStatThreads / 32) {
+        const int j = c0 + cc;  // 0-based Xt row
+        if (j >= m) break;
+        const float mu = mus[cc], sc = mus[kStatTile + cc];
+#pragma unroll
+        for (int e = 0; e < kStatTile / 32; ++e) {
+          const int r = lane + 32 * e, i = r0 + r;
+          if (i < n) {
+            float x = t[r * kStatPitch + cc] - mu;
+            if constexpr (kCorr) x /= sc;
+            xt[(size_t)j * ldx + i] = x;
+            xt_lo[(size_t)j * ldx + i] = x - tma::trunc_tf32(x);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // symmat[1 + r][1 + c] = G[min(r,c)][max(r,c)] (pitch ldg) (only G's upper
 // triangle is computed); CORR's diagonal is 1.  Block (32, 8), 64x64 tile.
 template <BenchId Bn, int V, bool kCorr>
@@ -330,11 +502,14 @@ inline void run(Workspace& ws, cudaStream_t s) {
       // pitch for the TMA maps, the K tail reads as zero), G (m x mp: split
       // 0's partial sums, or the whole Gram for the scatter fallback), then
       // the fp64 column sums and the per-column-block arrival counters
-      const int mp = (m + 3) / 4 * 4, np = (n + 3) / 4 * 4;
+      const int mp = (m + 3) / 4 * 4, np = (n + 7) / 8 * 8;
       const size_t xs = (size_t)m * np, gs = (size_t)m * mp;
       const int gx = (int)cdiv(m, 256);
+      const int rt = (int)cdiv(n, kStatTile), ntiles = rt * (int)cdiv(m, kStatTile);
+      const size_t part_doubles = 2 * (size_t)rt * m;
       float* X = ws.ensure_scratch((2 * xs + gs) * sizeof(float) + 2 * (m + 1) * sizeof(double) + 64 * 4 +
-                                   gx * sizeof(unsigned));
+                                   gx * sizeof(unsigned) + part_doubles * sizeof(double) + 256 +
+                                   (ntiles + 64) * sizeof(float));
       if (!X) {
         launch_failed("CORR/COVAR stage 2: scratch allocation failed");
         return;
@@ -343,17 +518,57 @@ inline void run(Workspace& ws, cudaStream_t s) {
       float* G = Xlo + xs;
       double* acc = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(G + gs) + 255) & ~uintptr_t(255));
       unsigned* arrivals = reinterpret_cast<unsigned*>(acc + 2 * (m + 1));
-      cudaMemsetAsync(acc, 0, 2 * (m + 1) * sizeof(double) + gx * sizeof(unsigned), s);
-      int splits = std::max(1, std::min((int)cdiv(device_sms() * 4, gx), (n + 31) / 32));
-      const int rps = (int)cdiv(n, splits);
-      splits = (int)cdiv(n, rps);
-      colstats_fused<Bn, V, kCorr><<<dim3(gx, splits), 256, 0, s>>>(data, acc, arrivals, mean, stdv, m, n, rps);
-      centre_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(data, mean, stdv, X,
-                                                                                            Xlo, m, n, np);
+      double* part = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(arrivals + gx) + 255) & ~uintptr_t(255));
+      float* f16_scale = reinterpret_cast<float*>(part + part_doubles);  // [2]
+      float* tmax = f16_scale + 64;                                      // [ntiles]
+      // one cooperative pass when every tile fits in the co-resident CTAs'
+      // shared memory (PF_CC_FUSED=0 forces the two-launch path, A/B runs);
+      // then the Gram runs on 3xFP16 images (PF_TC_F16=0: 3xTF32)
+      static const bool fused_ok = [] {
+        const char* e = std::getenv("PF_CC_FUSED");
+        return !(e && e[0] == '0');
+      }();
+      const int sms = device_sms();
+      int* flags = fused_ok ? ws.ensure_tile_flags(s) : nullptr;
+      const bool f16 = tc_f16_enabled() && m >= 256;
+      const void* coop = f16 ? (const void*)stats_centre_coop<Bn, V, kCorr, true>
+                             : (const void*)stats_centre_coop<Bn, V, kCorr, false>;
+      const bool fused = flags && occupancy(coop, kStatThreads, kStatSmem) >= 1 && ntiles <= kStatTiles * sms;
+      F16Operands f16ops;
+      if (fused) {
+        const int grid = std::min(ntiles, sms);
+        int epoch = ++ws.tile_epoch;
+        void* xh = X;
+        void* xl = f16 ? (void*)(reinterpret_cast<__half*>(X) + xs) : (void*)Xlo;
+        void* args[] = {(void*)&data, (void*)&part, (void*)&tmax, (void*)&flags, (void*)&epoch, (void*)&mean,
+                        (void*)&stdv, (void*)&xh, (void*)&xl, (void*)&f16_scale, (void*)&m, (void*)&n, (void*)&np};
+        if (cudaLaunchCooperativeKernel(coop, dim3(grid), dim3(kStatThreads), args, kStatSmem, s) != cudaSuccess) {
+          launch_failed("CORR/COVAR stage 2: cooperative statistics launch rejected");
+          return;
+        }
+        f16ops.hi[0] = f16ops.hi[1] = xh;
+        f16ops.lo[0] = f16ops.lo[1] = xl;
+        f16ops.hi[2] = f16ops.hi[3] = f16ops.lo[2] = f16ops.lo[3] = nullptr;
+        f16ops.kp = np;
+        f16ops.scale = f16_scale;
+        f16ops.sb = 0;
+      } else {
+        cudaMemsetAsync(acc, 0, 2 * (m + 1) * sizeof(double) + gx * sizeof(unsigned), s);
+        int splits = std::max(1, std::min((int)cdiv(sms * 4, gx), (n + 31) / 32));
+        const int rps = (int)cdiv(n, splits);
+        splits = (int)cdiv(n, rps);
+        colstats_fused<Bn, V, kCorr><<<dim3(gx, splits), 256, 0, s>>>(data, acc, arrivals, mean, stdv, m, n, rps);
+        centre_transpose<Bn, V, kCorr><<<dim3(cdiv(m, kCT), cdiv(n, kCT)), dim3(32, 8), 0, s>>>(data, mean, stdv, X,
+                                                                                              Xlo, m, n, np);
+      }
       // Xt Xt^T with K-major operands
       TcGemmArgs g{m, m, n, 1.f, 0.f, X, np, false, X, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
-      g.Alo = Xlo;
-      g.Blo = Xlo;
+      if (fused && f16) {
+        g.f16 = &f16ops;
+      } else {
+        g.Alo = Xlo;
+        g.Blo = Xlo;
+      }
       g.tile_flags = ws.ensure_tile_flags(s);
       g.epoch = ++ws.tile_epoch;
       if (!launch_tc_tma<Bn, V>(g, s)) {
@@ -383,7 +598,10 @@ inline void run(Workspace& ws, cudaStream_t s) {
 inline int64_t launches(bool corr, int stage, int64_t m, int64_t n) {
   if (stage == 0) return corr ? 4 : 3;
   const int64_t stats = corr ? 4 : 2;
-  if (stage == 2) return 2 + tc_tma_launches(m, m, n, false, true, true) + 1;  // stats, centre, Gram, scatter
+  if (stage == 2) {  // [stats + centre fused | stats, centre], Gram, scatter
+    const int64_t tiles = cdiv(m, kStatTile) * cdiv(n, kStatTile);
+    return (tiles <= kStatTiles * device_sms() ? 1 : 2) + tc_tma_launches(m, m, n, false, true, true) + 1;
+  }
   return stats + 1 + 1 + 1 + (corr ? 1 : 0);
 }
 

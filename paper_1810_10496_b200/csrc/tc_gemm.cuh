@@ -29,6 +29,17 @@
 
 namespace pf {
 
+// 3xFP16 operands (tc_f16.cuh): x * s = hi + lo with hi = fp16_rn(x s),
+// lo = fp16_rn(x s - hi), s a power of two per operand group putting
+// max|x s| in [2^14, 2^15); images are K-major R x kp halfs.
+struct F16Operands {
+  const void* hi[4];   // op(A), op(B), op(A2), op(B2)
+  const void* lo[4];
+  int kp;              // image pitch (halfs, multiple of 8)
+  const float* scale;  // device [2]: scale of A's group, of B's group
+  int sb;              // index of B's scale (0: one scale for all operands)
+};
+
 struct TcGemmArgs {
   int M, N, K;
   float alpha, beta;
@@ -62,6 +73,8 @@ struct TcGemmArgs {
   // on or above the diagonal are computed; off-diagonal tiles are also
   // added, transposed, below the diagonal (beta pre-pass + add-reductions)
   int sym = 0;
+  // 3xFP16 operand images (nullptr: fp32 operands, 3xTF32)
+  const F16Operands* f16 = nullptr;
 };
 
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;
@@ -164,6 +177,17 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// kind::f16 (fp16 A/B, fp32 accumulate; K = 16 per instruction = 32 bytes,
+// the same byte step as kind::tf32's K = 8)
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }

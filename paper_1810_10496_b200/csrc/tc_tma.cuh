@@ -71,6 +71,9 @@ struct TmaParams {
   int upper_only;
   uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides / k-step advance (bytes)
   int idesc_override;                 // probe only: -1 auto, else (a_major | b_major << 1)
+  int f16;                            // operands are 3xFP16 images (hi/lo fp16, K-major): kind::f16 MMAs
+  const float* f16_scale;             // f16: power-of-two operand scales [A group, B group]; alpha / (sA sB)
+  int f16_sb;                         // f16: index of B's scale in f16_scale
   int diag;                           // diagnostics only (PF_TC_DIAG): 1 skip lo split, 2 skip MMAs, 4 skip loads, 8 skip epilogue, 16 lane-row epilogue, 32 smem-transpose epilogue
 };
 
@@ -119,9 +122,17 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr, bool mn_major, uint32_t
   return d;
 }
 
-__device__ __forceinline__ uint32_t idesc(int m, int n, int a_mn, int b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+// D f32 (bit 4); A/B format @7 / @10: tf32 = 2 (kind::tf32), f16 = 0 (kind::f16)
+__device__ __forceinline__ uint32_t idesc(int m, int n, int a_mn, int b_mn, bool f16 = false) {
+  const uint32_t fmt = f16 ? 0u : 2u;
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+// Effective alpha of the epilogue: 3xFP16 operands were scaled by powers of
+// two, undone here exactly.
+__device__ __forceinline__ float eff_alpha(const TmaParams& p) {
+  return p.f16 ? p.alpha / (__ldg(p.f16_scale) * __ldg(p.f16_scale + p.f16_sb)) : p.alpha;
 }
 
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
@@ -179,8 +190,8 @@ __device__ __forceinline__ void reduce_add_2d(const CUtensorMap* map, uint32_t s
 // 16 * (j ^ (row % 8)), conflict-free -- and written back by one TMA store
 // (or a TMA add-reduction onto the beta-prescaled D for split-K).  buf:
 // 1024-byte aligned, ncols / 32 * 4 KB; bar: this warp's mbarrier (phase 0).
-__device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr, int ncols, int row0, int col0,
-                                             bool split, uint8_t* buf, uint32_t bar, int lane,
+__device__ __forceinline__ void epilogue_tma(const TmaParams& p, float alpha, uint32_t taddr, int ncols, int row0,
+                                             int col0, bool split, uint8_t* buf, uint32_t bar, int lane,
                                              bool writes_done = false, uint8_t* lobuf = nullptr,
                                              bool mirror = false) {
   if (row0 >= p.M) return;  // warp-uniform
@@ -203,8 +214,8 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, uint32_t taddr,
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float4* slot = row + (j ^ (lane & 7));
-      float4 v = make_float4(p.alpha * __uint_as_float(r[4 * j]), p.alpha * __uint_as_float(r[4 * j + 1]),
-                             p.alpha * __uint_as_float(r[4 * j + 2]), p.alpha * __uint_as_float(r[4 * j + 3]));
+      float4 v = make_float4(alpha * __uint_as_float(r[4 * j]), alpha * __uint_as_float(r[4 * j + 1]),
+                             alpha * __uint_as_float(r[4 * j + 2]), alpha * __uint_as_float(r[4 * j + 3]));
       if (use_c) {
         const float4 ci = *slot;
         v = make_float4(fmaf(p.beta, ci.x, v.x), fmaf(p.beta, ci.y, v.y), fmaf(p.beta, ci.z, v.z),
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
         }
         tc::mbar_expect_tx(fb, (p.presplit ? 4 : 2) * kTmaTileBytes);
         const bool second = kb >= p.kb1;
-        const int k0 = (second ? kb - p.kb1 : kb) * 32;
+        const int k0 = (second ? kb - p.kb1 : kb) * (p.f16 ? 64 : 32);  // elements per 128-byte k block
         const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
         tma::load_operands(p, second, false, base, m0, n0, k0, fb);
         if (p.presplit) tma::load_operands(p, second, true, base + 2 * kTmaTileBytes, m0, n0, k0, fb);
@@ -365,7 +376,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t id = p.idesc_override < 0 ? tma::idesc(128, 128, p.a_mn, p.b_mn)
+      const uint32_t id = p.idesc_override < 0 ? tma::idesc(128, 128, p.a_mn, p.b_mn, p.f16)
                                                : tma::idesc(128, 128, p.idesc_override & 1, p.idesc_override >> 1);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kTmaStages;
@@ -383,9 +394,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
           const uint64_t alo = tma::desc(base + 2 * kTmaTileBytes + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
           const uint64_t blo = tma::desc(base + 3 * kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
           if (p.diag & 2) continue;
-          tc::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
-          tc::mma_tf32(tmem, ahi, blo, id, 1u);
-          tc::mma_tf32(tmem, ahi, bhi, id, 1u);
+          if (p.f16) {
+            tc::mma_f16(tmem, alo, bhi, id, (i | kk) != 0);
+            tc::mma_f16(tmem, ahi, blo, id, 1u);
+            tc::mma_f16(tmem, ahi, bhi, id, 1u);
+          } else {
+            tc::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
+            tc::mma_tf32(tmem, ahi, blo, id, 1u);
+            tc::mma_tf32(tmem, ahi, bhi, id, 1u);
+          }
         }
         tc::mma_commit(tc::smem_u32(&empty_bar[s]));
       }
@@ -415,17 +432,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
-      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
+      tma::epilogue_tma(p, tma::eff_alpha(p), tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
                         p.sym && nb != mb);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
-      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
                              p.Cin, p.ldc, p.D, p.ldd, split, lane);
     else if (!(p.diag & 8))
-      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
                           p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
   }
   tc::fence_before();
@@ -501,6 +518,15 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       : "memory");
 }
 
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 __device__ __forceinline__ void commit_both(uint32_t bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
@@ -564,7 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
           continue;
         }
         const bool second = kb >= p.kb1;
-        const int k0 = (second ? kb - p.kb1 : kb) * 32;
+        const int k0 = (second ? kb - p.kb1 : kb) * (p.f16 ? 64 : 32);  // elements per 128-byte k block
         const uint32_t base = tc::smem_u32(smem + (size_t)s * kTmaStageBytes);
         if (p.presplit) {
           // both CTAs' bytes complete on the LEADER's full[s]: its MMA issuer
@@ -582,7 +608,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      const uint32_t id = tma::idesc(256, 256, p.a_mn, p.b_mn);
+      const uint32_t id = tma::idesc(256, 256, p.a_mn, p.b_mn, p.f16);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kTmaStages;
         const uint32_t ph = (i / kTmaStages) & 1;
@@ -598,9 +624,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
           const uint64_t alo = tma::desc(base + 2 * kTmaTileBytes + ka, p.a_mn, p.mn_lbo, p.mn_sbo);
           const uint64_t blo = tma::desc(base + 3 * kTmaTileBytes + kbo, p.b_mn, p.mn_lbo, p.mn_sbo);
           if (p.diag & 2) continue;
-          tc2::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
-          tc2::mma_tf32(tmem, ahi, blo, id, 1u);
-          tc2::mma_tf32(tmem, ahi, bhi, id, 1u);
+          if (p.f16) {
+            tc2::mma_f16(tmem, alo, bhi, id, (i | kk) != 0);
+            tc2::mma_f16(tmem, ahi, blo, id, 1u);
+            tc2::mma_f16(tmem, ahi, bhi, id, 1u);
+          } else {
+            tc2::mma_tf32(tmem, alo, bhi, id, (i | kk) != 0);
+            tc2::mma_tf32(tmem, ahi, blo, id, 1u);
+            tc2::mma_tf32(tmem, ahi, bhi, id, 1u);
+          }
         }
         tc2::commit_both(tc::smem_u32(&empty_bar[s]));
       }
@@ -629,17 +661,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
-      tma::epilogue_tma(p, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
+      tma::epilogue_tma(p, tma::eff_alpha(p), tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
                         p.sym && nb != mb);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
-      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
                              p.Cin, p.ldc, p.D, p.ldd, split, lane);
     else if (!(p.diag & 8))
-      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
+      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
                           p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
   }
   tc::fence_before();
@@ -655,28 +687,28 @@ namespace tma {
 // 2-D fp32 tensor map over X[outer][inner] (row pitch ld elements), box
 // {box_inner, box_outer}, out-of-bounds reads as zero.  K-major tiles use
 // SWIZZLE_128B, MN-major tiles SWIZZLE_128B_ATOM_32B (see desc()).
-inline bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, int64_t ld, uint32_t box_inner,
-                     uint32_t box_outer, bool base32) {
+inline bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, uint32_t box_inner,
+                     uint32_t box_outer, bool base32, bool f16 = false) {
   struct Key {
-    const float* p;
+    const void* p;
     int64_t a, b, c;
     uint32_t d, e;
-    bool f;
+    bool f, h;
     bool operator==(const Key& o) const {
-      return p == o.p && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e && f == o.f;
+      return p == o.p && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e && f == o.f && h == o.h;
     }
   };
   struct Hash {
     size_t operator()(const Key& k) const {
       size_t h = std::hash<const void*>()(k.p);
-      for (int64_t v : {k.a, k.b, k.c, (int64_t)k.d, (int64_t)k.e, (int64_t)k.f})
+      for (int64_t v : {k.a, k.b, k.c, (int64_t)k.d, (int64_t)k.e, (int64_t)k.f, (int64_t)k.h})
         h = h * 1000003u ^ std::hash<int64_t>()(v);
       return h;
     }
   };
   static std::mutex mu;
   static std::unordered_map<Key, CUtensorMap, Hash> cache;
-  const Key key{ptr, inner, outer, ld, box_inner, box_outer, base32};
+  const Key key{ptr, inner, outer, ld, box_inner, box_outer, base32, f16};
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -686,10 +718,11 @@ inline bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t 
   EncodeFn enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4u};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * (f16 ? 2u : 4u)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+  CUresult r = enc(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
                    base32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -703,6 +736,14 @@ inline bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t 
 inline bool operand_map(CUtensorMap* map, const float* X, bool mn_major, int64_t R, int64_t K, int64_t ld) {
   if (reinterpret_cast<uintptr_t>(X) % 16 || (ld * 4) % 16) return false;
   return mn_major ? make_map(map, X, R, K, ld, 32, 32, true) : make_map(map, X, K, R, ld, 32, 128, false);
+}
+
+// 3xFP16 operand image (K-major R x K halfs, pitch ld): 128 rows x 64 halfs
+// (128-byte rows, SWIZZLE_128B) -- byte-identical shared-memory layout to
+// the fp32 K-major tile, so the same UMMA descriptors apply.
+inline bool operand_map_f16(CUtensorMap* map, const void* X, int64_t R, int64_t K, int64_t ld) {
+  if (reinterpret_cast<uintptr_t>(X) % 16 || (ld * 2) % 16) return false;
+  return make_map(map, X, K, R, ld, 64, 128, false, true);
 }
 
 }  // namespace tma
@@ -721,6 +762,7 @@ inline TmaProbe& tma_probe() {
 }  // namespace pf
 
 #include "tc_splitk.cuh"  // small products: split-K in a cluster (needs the map helpers above)
+#include "tc_f16.cuh"     // 3xFP16 operand images
 
 namespace pf {
 
@@ -759,7 +801,7 @@ template <BenchId Bn, int V>
 inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written = nullptr) {
   if (dlo_written) *dlo_written = false;
   // small single products: split-K inside a cluster, DSMEM reduction (one launch)
-  if (!a.sym && !a.upper_only && !a.A2 && launch_tc_splitk<Bn, V>(a, s)) return true;
+  if (!a.f16 && !a.sym && !a.upper_only && !a.A2 && launch_tc_splitk<Bn, V>(a, s)) return true;
   TmaParams p;
   std::memset(&p, 0, sizeof(p));
   p.mn_lbo = tma_probe().lbo;
@@ -771,6 +813,28 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
     return e ? std::atoi(e) : 0;
   }();
   p.diag = diag;
+  if (a.f16) {
+    // 3xFP16: K-major fp16 hi / lo images for every operand (tc_f16.cuh)
+    const F16Operands& f = *a.f16;
+    p.f16 = 1;
+    p.f16_scale = f.scale;
+    p.f16_sb = f.sb;
+    p.presplit = 1;
+    if (!tma::operand_map_f16(&p.ta, f.hi[0], a.M, a.K, f.kp) || !tma::operand_map_f16(&p.tal, f.lo[0], a.M, a.K, f.kp) ||
+        !tma::operand_map_f16(&p.tb, f.hi[1], a.N, a.K, f.kp) || !tma::operand_map_f16(&p.tbl, f.lo[1], a.N, a.K, f.kp))
+      return false;
+    if (a.A2) {
+      if (!tma::operand_map_f16(&p.ta2, f.hi[2], a.M, a.K, f.kp) ||
+          !tma::operand_map_f16(&p.ta2l, f.lo[2], a.M, a.K, f.kp) ||
+          !tma::operand_map_f16(&p.tb2, f.hi[3], a.N, a.K, f.kp) || !tma::operand_map_f16(&p.tb2l, f.lo[3], a.N, a.K, f.kp))
+        return false;
+    } else {
+      p.ta2 = p.ta;
+      p.tb2 = p.tb;
+      p.ta2l = p.tal;
+      p.tb2l = p.tbl;
+    }
+  } else {
   p.a_mn = a.ta ? 1 : 0;
   p.b_mn = a.tb ? 0 : 1;
   if (!tma::operand_map(&p.ta, a.A, p.a_mn, a.M, a.K, a.lda)) return false;
@@ -791,6 +855,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
     p.ta2l = p.tal;
     p.tb2l = p.tbl;
   }
+  }
   // TMA epilogue when D (and Cin, if read) are 16-byte aligned with 16-byte pitches
   p.tma_epi = (reinterpret_cast<uintptr_t>(a.D) % 16 == 0 && (a.ldd * 4) % 16 == 0 &&
                tma::make_map(&p.td, a.D, a.N, a.M, a.ldd, 32, 32, false))
@@ -801,7 +866,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
                  tma::make_map(&p.tc, a.Cin, a.N, a.M, a.ldc, 32, 32, false))
                     ? 1
                     : 0;
-  const int kb1 = (a.K + 31) / 32;
+  const int kb1 = a.f16 ? (a.K + 63) / 64 : (a.K + 31) / 32;  // 128-byte k blocks
   const int kblocks = a.A2 ? 2 * kb1 : kb1;
   // split-K problems: beta pre-pass + TMA add-reductions, or the ordered
   // hand-over for beta = 0.  (Reducing the partials inside a z-cluster through
@@ -816,7 +881,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   const bool pair = tc_pair_ok(a.M, a.N) && tc_tma_splits(a.M, a.N, kblocks, true, up) <= 2;
   const int zs = tc_tma_splits(a.M, a.N, kblocks, pair, up);
   const int per = (kblocks + zs - 1) / zs;
-  p.dlo = (a.Dlo && p.tma_epi && zs == 1 && !p.sym && reinterpret_cast<uintptr_t>(a.Dlo) % 16 == 0 &&
+  p.dlo = (a.Dlo && !a.f16 && p.tma_epi && zs == 1 && !p.sym && reinterpret_cast<uintptr_t>(a.Dlo) % 16 == 0 &&
            tma::make_map(&p.tdl, a.Dlo, a.N, a.M, a.ldd, 32, 32, false))
               ? 1
               : 0;
@@ -825,7 +890,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   // ordered hand-over only where the alternative pre-pass is a memset (beta
   // == 0): with beta != 0 split 0's Cin load + store serialise the splits
   // (GEMM 512^3: 17.4 us vs 15.3 us with the beta pre-pass)
-  const bool ordered = zs > 1 && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlags &&
+  const bool ordered = zs > 1 && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlagsGemm &&
                        a.beta == 0.f;
   const bool prepass = (zs > 1 || p.sym) && !ordered;  // beta * Cin (or zero) before the adds
   p.tile_flags = ordered ? a.tile_flags : nullptr;
@@ -944,10 +1009,29 @@ inline bool tc_presplit_wanted(int64_t m, int64_t n, int64_t k, bool dual, bool 
   return tc_tma_splits(m, n, kblocks, pair, upper) == 1;
 }
 
+// 3xFP16 for the products that run pre-split (large enough for CTA pairs
+// or symmetric), when the fp16 images fit the 16-byte TMA pitch rules
+inline bool tc_f16_wanted(int64_t m, int64_t n, int64_t k, bool dual, bool upper, bool sym) {
+  return tc_f16_enabled() && m >= 256 && n >= 256 && (sym || tc_presplit_wanted(m, n, k, dual, upper));
+}
+inline bool tc_f16_wanted(const TcGemmArgs& a) {
+  return tc_f16_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0, a.sym != 0);
+}
+
+// launches of a 3xFP16 contraction: absmax + split + [beta pre-pass] + gemm
+inline int64_t tc_f16_launches(int64_t m, int64_t n, int64_t k, bool dual, bool sym, bool beta_zero = false) {
+  if (sym) return 4;
+  const int kblocks = (int)((dual ? 2 : 1) * ((k + 63) / 64));
+  const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, false) <= 2;
+  const bool split = tc_tma_splits(m, n, kblocks, pair, false) > 1;
+  return 2 + 1 + (split && !beta_zero ? 1 : 0);
+}
+
 // launches of one contraction: [lo passes, one per distinct operand array] +
-// [prescale] + gemm (TMA path) or the packed path's sequence
+// [prescale] + gemm (TMA path), the 3xFP16 sequence, or the packed path's
 inline int64_t tc_launches(int64_t m, int64_t n, int64_t k, bool tma, bool dual, int operands) {
   if (!tma) return tc_gemm_launches(m, n, k, dual);
+  if (tc_f16_wanted(m, n, k, dual, false, false)) return tc_f16_launches(m, n, k, dual, false);
   return tc_tma_launches(m, n, k, dual) + (tc_presplit_wanted(m, n, k, dual, false) ? operands : 0);
 }
 
@@ -960,6 +1044,17 @@ inline bool launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t
   a.tile_flags = ws.ensure_tile_flags(s);
   a.epoch = ++ws.tile_epoch;
   bool dlo = false;
+  // 3xFP16 operand images for the products that would run pre-split
+  if (tc_f16_wanted(a)) {
+    F16Operands f;
+    if (prepare_f16<Bn, V>(ws, a, f, s)) {
+      TcGemmArgs b = a;
+      b.f16 = &f;
+      b.Alo = b.Blo = b.A2lo = b.B2lo = nullptr;
+      b.Dlo = nullptr;
+      if (launch_tc_tma<Bn, V>(b, s)) return false;
+    }
+  }
   // symmetric products split-K their upper tiles but still profit from the
   // pre-split operands (SYRK: one lo pass serves both operands)
   if ((a.sym || tc_presplit_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0)) && tma_ok(a.lda, a.ldb)) {

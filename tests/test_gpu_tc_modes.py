@@ -1,0 +1,108 @@
+"""The two tensor-core arithmetic modes of the stage-2 contractions.
+
+* 3xFP16 (default for products that run pre-split, tc_f16.cuh): operands are
+  scaled by a power of two and split into fp16 hi / lo images.  Its scaling
+  is exercised here with inputs spanning many decades and both signs (the
+  PolyBench inputs are all O(1)), against an fp64 numpy product, at sizes
+  where the f16 path is taken (SYRK from n = 256; plain products from ~1.6k).
+* 3xTF32 (PF_TC_F16=0) and the two-launch CORR/COVAR statistics
+  (PF_CC_FUSED=0) stay available for A/B runs: the tensor-core parity tests
+  are re-run in a subprocess with both switches off.
+
+Tolerance as everywhere: |t - r| <= max(1e-4 max|r|, 1e-4 |r|).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+RTOL = 1e-4
+
+
+def _check(got, ref):
+    ref = ref.astype(np.float64)
+    tol = np.maximum(RTOL * np.abs(ref).max(), RTOL * np.abs(ref))
+    err = np.abs(got.astype(np.float64) - ref)
+    worst = float((err / tol).max())
+    assert worst <= 1.0, f"max error / tolerance = {worst:.3g}"
+    return worst
+
+
+def _wide(rng, shape, decades=8):
+    mag = 10.0 ** rng.uniform(-decades / 2, decades / 2, size=shape)
+    return (mag * rng.choice([-1.0, 1.0], size=shape)).astype(np.float32)
+
+
+def _stage2(bench):
+    from paper_1810_10496_b200.backend.b200 import family
+
+    fam = family(bench)
+    return next(v for v in range(len(fam.knobs)) if fam.key(v) == "stage=2")
+
+
+def _run(bench, dims, inputs):
+    from paper_1810_10496_b200.backend.b200 import Workspace
+
+    ws = Workspace(0, bench, dims)
+    try:
+        ws.generate(True, 1729, -1)
+        for a, x in inputs.items():
+            ws.upload(a, x)
+        ws.run(_stage2(bench), samples=1, batch=1, restore=False, flush=False)
+        return [ws.download(a) for a, (_, _, o) in enumerate(ws.arrays) if o]
+    finally:
+        ws.close()
+
+
+@pytest.mark.parametrize("n,m", [(384, 320), (1024, 520)])
+def test_syrk_wide_range(n, m):
+    rng = np.random.default_rng(n + m)
+    A = _wide(rng, (n, m))
+    C = _wide(rng, (n, n), decades=2)
+    (out,) = _run("SYRK", (n, m), {0: A, 1: C})
+    a64 = A.astype(np.float64)
+    ref = 12435.0 * (a64 @ a64.T) + 4546.0 * C.astype(np.float64)
+    _check(out, ref)
+
+
+def test_2mm_wide_range_f16_path():
+    n = 1792  # plain products fill the GPU without split-K from here: the 3xFP16 path
+    rng = np.random.default_rng(3)
+    A = _wide(rng, (n, n), 6)
+    B = _wide(rng, (n, n), 6)
+    D = _wide(rng, (n, n), 4)
+    outs = _run("2MM", (n, n, n, n), {0: A, 1: B, 3: D})
+    C_ref = A.astype(np.float64) @ B.astype(np.float64)
+    _check(outs[0], C_ref)
+    E_ref = outs[0].astype(np.float64) @ D.astype(np.float64)  # second product on the device's C
+    _check(outs[1], E_ref)
+
+
+def test_syr2k_wide_range():
+    n, m = 512, 448
+    rng = np.random.default_rng(7)
+    A = _wide(rng, (n, m), 6)
+    B = _wide(rng, (n, m), 3)  # different magnitudes: one shared scale for both pairs
+    C = _wide(rng, (n, n), 2)
+    (out,) = _run("SYR2K", (n, m), {0: A, 1: B, 2: C})
+    a, b = A.astype(np.float64), B.astype(np.float64)
+    ref = 12435.0 * (a @ b.T + b @ a.T) + 4546.0 * C.astype(np.float64)
+    _check(out, ref)
+
+
+def test_tf32_mode_and_unfused_statistics_still_match():
+    env = dict(os.environ, PF_TC_F16="0", PF_CC_FUSED="0")
+    env.pop("PF_PARITY_LOG", None)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_parity.py", "-k", "tensor_core"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
