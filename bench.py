@@ -346,6 +346,9 @@ def run_gpu(args, dist: Dist) -> int:
         for st in keep:
             st.free()
 
+    # ---- BASELINE configs[4] sample: explore() over all 15 kernels at their config sizes
+    sweep = sweep_sample(be, args.sweep_orders, dist) if args.sweep_orders > 0 else None
+
     # ---- per-kernel report (outside the timed region)
     report = {}
     for c in cases:
@@ -399,6 +402,7 @@ def run_gpu(args, dist: Dist) -> int:
             "per_kernel": report,
             "roofline": roofline,
             "e2e": e2e,
+            "sweep": sweep,
             "cpu_baseline": cpu,
             "gpu_launches": n_launch,
             "clocks": clocks.summary(),
@@ -406,6 +410,47 @@ def run_gpu(args, dist: Dist) -> int:
         print(json.dumps(line), flush=True)
     be.close()
     return 0
+
+
+# per-kernel seconds of the B200 full sweep (profiles/r02_campaign_staging): LPT weights for sharding the
+# configs[4] sample's kernels over ranks (all timed runs of a kernel stay on one device)
+SWEEP_COSTS = {"2DCONV": 1, "3DCONV": 3, "2MM": 12, "3MM": 15, "ATAX": 6, "BICG": 6, "CORR": 138, "COVAR": 142,
+               "FDTD-2D": 12, "GEMM": 1, "GESUMMV": 4, "GRAMSCHM": 846, "MVT": 6, "SYR2K": 28, "SYRK": 21}
+
+
+def sweep_sample(be, orders: int, dist: Dist) -> dict:
+    """A bounded sample of BASELINE configs[4] (the full 15-kernel sweep):
+    ``explore()`` on every kernel at its config size over an ``orders``-long
+    stream through the same product path (compile, digest dedup, validation
+    + compare, one measurement per fresh artifact), kernels sharded over the
+    ranks by LPT with device affinity.  The whole sweep with finalize /
+    reduce_order / LOO (1000 orders, ~21 min on one B200) is
+    tools/run_campaign.py (profiles/r02_campaign_*)."""
+    from paper_1810_10496_b200 import passmodel, registry
+    from paper_1810_10496_b200.campaign import kernel_config, kernel_owners
+    from paper_1810_10496_b200.explorer import ExplorationConfig, RecordStatus
+    from paper_1810_10496_b200.sweep import explore_suite
+
+    kernels = [registry.kernel_case(b, "config") for b in registry.BENCHES]
+    owners = kernel_owners(kernels, dist.world, SWEEP_COSTS)
+    mine = registry.build_suite(be, size="config",
+                                benches=[k.id for k, o in zip(kernels, owners) if o == dist.rank])
+    base = ExplorationConfig(num_sequences=orders, max_len=256)
+    cfgs = [replace(kernel_config(base, c), seed=4242 + i) for i, c in enumerate(mine)]
+    timer = StepTimer()
+    dist.barrier()
+    with timer:
+        out = explore_suite(mine, passmodel.default_catalog(), cfgs, be)
+    dist.barrier()
+    fresh = sum(1 for v in out.values() for r in v if r.status not in (RecordStatus.REUSED, RecordStatus.NO_IR))
+    records = sum(len(v) for v in out.values())
+    seconds = dist.max(timer.ms / 1e3)
+    total_fresh = dist.sum(fresh)
+    return {"workload": f"BASELINE configs[4] sample: explore() on all 15 kernels at config sizes, {orders} orders "
+                        "each (default catalog, max_len 256)",
+            "value": total_fresh / seconds, "unit": "evals/s", "fresh_evaluations": total_fresh,
+            "records": dist.sum(records), "seconds": seconds, "scaling": "strong (kernels sharded over ranks)",
+            "timing": "CUDA events around the whole explore() sample after a device synchronize, max over ranks"}
 
 
 def ncu_traffic(bench: str, variant: int):
@@ -432,6 +477,8 @@ def main() -> int:
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-orders", type=int, default=2, help="orders per kernel in the cpu_baseline sample")
     ap.add_argument("--ref-orders", type=int, default=2, help="orders per kernel per step of --impl reference")
+    ap.add_argument("--sweep-orders", type=int, default=100,
+                    help="orders per kernel of the configs[4] sample (explore() on all 15 kernels); 0: skip")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the roofline kernel from an ncu --set full capture")
     args = ap.parse_args()

@@ -8,7 +8,11 @@
 //          the paper's 5.4x CORR case).
 // stage 1  row-split column statistics (atomics) and the Gram matrix D^T D
 //          as an upper-triangle tiled SIMT GEMM + mirror.
-// stage 2  four launches: (1) one pass over data accumulates every column's
+// stage 2  3xFP16 Gram (m >= 256, n <= kCSMaxRows): three launches -- the
+//          column-strip kernel (statistics, centring, per-column scaled fp16
+//          hi/lo operand rows; strip_stats_f16), the Gram on kind::f16 pair
+//          tiles, the scatter.  Otherwise (3xTF32)
+//          four launches: (1) one pass over data accumulates every column's
 //          sum and sum of squares in fp64 (row splits, fp64 atomics) and the
 //          last block of each column finishes mean (and CORR's std) --
 //          sum (x - mu)^2 = S2 - 2 mu S1 + n mu^2 exactly in fp64; (2) the
@@ -275,175 +279,121 @@ __global__ void __launch_bounds__(256) centre_transpose(const float* __restrict_
     }
 }
 
-// ---- stage 2, fused: column statistics + centre/scale + transpose + lo
-// split in ONE cooperative launch (replaces colstats_fused + centre_transpose:
-// the data is read from HBM once and never re-read).  The data is cut into
-// 128 x 128 tiles; each CTA (one per SM) loads up to kStatTiles of them into
-// shared memory while accumulating per-thread fp64 column sums, writes its
-// per-tile column partials P[row tile][col] (no atomics, every slot written
-// exactly once), passes a grid barrier, sums the row-tile partials of its
-// columns in a fixed order (deterministic), and writes the centred (scaled)
-// tile transposed into Xt / Xt_lo straight from shared memory.  The float
-// arithmetic of mean / std / x' is exactly colstats_fused + centre_transpose's.
-constexpr int kStatTile = 128, kStatTiles = 2, kStatThreads = 256;
-constexpr int kStatPitch = kStatTile + 1;  // conflict-free column reads
-constexpr size_t kStatSmem = (size_t)kStatTiles * kStatTile * kStatPitch * sizeof(float) + 2 * 2 * kStatTile * sizeof(double);
+// ---- stage 2 (3xFP16 Gram): column statistics + centre/scale + operand
+// split in ONE launch with no inter-CTA dependency.  A CTA owns a strip of
+// kCS whole columns: all n rows of the strip land in shared memory through
+// cp.async (every 4-byte load in flight at once, no registers), the fp64
+// column sums and the mean / std are exact per CTA (sum (x - mu)^2 =
+// S2 - 2 mu S1 + n mu^2 as before), the centred (scaled) column gets its own
+// power-of-two scale from its max|x'|, and each column leaves as one K-major
+// row of the Gram operand: n fp16 hi + n fp16 lo halfs, coalesced.  Data
+// is read from HBM once; the Gram epilogue undoes the column scales.
+constexpr int kCS = 16;              // columns per CTA
+constexpr int kCSThreads = 256;      // 16 columns x 16 row groups
+constexpr int kCSMaxRows = 2944;     // n * (kCS + 1) * 4 bytes <= 200 KB of shared memory
 
-// kF16: the Gram runs on 3xFP16 images (tc_f16.cuh) -- xt / xt_lo are fp16
-// hi / lo images of x' * s, s = scale_of(bound) written to scale[0], with
-// bound = 2 (CORR: |x'| <= 1 since sum_i x'^2 = 1, or <= 0.005 for clamped
-// columns) or 2 max|data| (COVAR: |x - mu| <= 2 max|x|); each tile's max|x|
-// goes to tmax[] in phase 1.  Else fp32 x' and its 3xTF32 lo image.
-template <BenchId Bn, int V, bool kCorr, bool kF16>
-__global__ void __launch_bounds__(kStatThreads, 1)
-    stats_centre_coop(const float* __restrict__ data, double* part, float* tmax, int* flags, int epoch, float* mean,
-                      float* stdv, void* __restrict__ xt_, void* __restrict__ xt_lo_, float* scale, int m, int n,
-                      int ldx) {
-  extern __shared__ float st_smem[];
-  __shared__ float bred[8];
-  double* red = reinterpret_cast<double*>(st_smem + kStatTiles * kStatTile * kStatPitch);  // [2][2][128]
-  const int ct = (m + kStatTile - 1) / kStatTile, rt = (n + kStatTile - 1) / kStatTile;
-  const int ntiles = ct * rt;
-  const int c = threadIdx.x & (kStatTile - 1), h = threadIdx.x >> 7;  // column, row parity
-  // ---- phase 1: loads (64 per thread per tile in flight) + column partials
-#pragma unroll 1
-  for (int q = 0; q < kStatTiles; ++q) {
-    const int tile = blockIdx.x + q * gridDim.x;
-    if (tile >= ntiles) break;
-    const int r0 = (tile / ct) * kStatTile, c0 = (tile % ct) * kStatTile;
-    float* t = st_smem + q * kStatTile * kStatPitch;
-    const int j = c0 + c + 1;
-    float v[kStatTile / 2];
-#pragma unroll
-    for (int e = 0; e < kStatTile / 2; ++e) {
-      const int i = r0 + h + 2 * e + 1;
-      v[e] = (i <= n && j <= m) ? __ldg(data + (size_t)i * (m + 1) + j) : 0.f;
+inline size_t strip_smem(int n) { return (size_t)n * (kCS + 1) * sizeof(float); }
+
+template <BenchId Bn, int V, bool kCorr>
+__global__ void __launch_bounds__(kCSThreads, 1)
+    strip_stats_f16(const float* __restrict__ data, float* mean, float* stdv, __half* __restrict__ xh,
+                    __half* __restrict__ xl, float* __restrict__ rinv, int m, int n, int ldx) {
+  extern __shared__ float cs_smem[];  // [n][kCS + 1]
+  __shared__ double r1[16][kCS], r2[16][kCS];
+  __shared__ float rmax[16][kCS], mus[kCS], scs[kCS], s16[kCS];
+  const int t = threadIdx.x, c = t % kCS, g = t / kCS;
+  const int j0 = blockIdx.x * kCS;  // 0-based first column of the strip
+  const int j = j0 + c + 1;         // 1-based data column of this thread
+  const bool colok = j <= m;
+  // ---- load: rows g, g + 16, ... of column c, straight into shared memory
+  {
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(cs_smem));
+    for (int i = g; i < n; i += 16) {
+      if (colok)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sbase + 4u * (uint32_t)(i * (kCS + 1) + c)),
+                     "l"(data + (size_t)(i + 1) * (m + 1) + j)
+                     : "memory");
+      else
+        cs_smem[i * (kCS + 1) + c] = 0.f;
     }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+  // ---- fp64 column sums (16 row groups, then a fixed-order combine)
+  {
     double s1 = 0.0, s2 = 0.0;
-    float vmax = 0.f;
-#pragma unroll
-    for (int e = 0; e < kStatTile / 2; e += 4) {
-      s1 += ((double)v[e] + v[e + 1]) + ((double)v[e + 2] + v[e + 3]);
-      if constexpr (kCorr)
-        s2 += ((double)v[e] * v[e] + (double)v[e + 1] * v[e + 1]) + ((double)v[e + 2] * v[e + 2] + (double)v[e + 3] * v[e + 3]);
-      if constexpr (kF16 && !kCorr)
-        vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(v[e]), fabsf(v[e + 1])), fmaxf(fabsf(v[e + 2]), fabsf(v[e + 3]))));
-    }
-#pragma unroll
-    for (int e = 0; e < kStatTile / 2; ++e) t[(h + 2 * e) * kStatPitch + c] = v[e];
-    red[(h * 2 + 0) * kStatTile + c] = s1;
-    if constexpr (kCorr) red[(h * 2 + 1) * kStatTile + c] = s2;
-    if constexpr (kF16 && !kCorr) {
-      vmax = f16op::block_max(vmax, bred);
-      if (threadIdx.x == 0) tmax[tile] = vmax;
-    }
-    __syncthreads();
-    if (h == 0 && j <= m) {
-      const size_t slot = (size_t)(r0 / kStatTile) * m + (j - 1);
-      part[slot] = red[c] + red[2 * kStatTile + c];
-      if constexpr (kCorr) part[(size_t)rt * m + slot] = red[kStatTile + c] + red[3 * kStatTile + c];
-    }
-    __syncthreads();
-  }
-  grid_barrier(flags, epoch);
-  float sc16 = 1.f;  // fp16 image scale
-  if constexpr (kF16) {
-    float bound = 2.f;
-    if constexpr (!kCorr) {
-      float mx = 0.f;
-      for (int k = threadIdx.x; k < ntiles; k += kStatThreads) mx = fmaxf(mx, __ldcg(tmax + k));
-      mx = f16op::block_max(mx, bred);
-      if (threadIdx.x == 0) bred[0] = mx;
-      __syncthreads();
-      bound = 2.f * bred[0];
-      __syncthreads();
-    }
-    sc16 = f16op::scale_of(bound);
-    if (blockIdx.x == 0 && threadIdx.x == 0) scale[0] = sc16;
-  }
-  // ---- phase 2: statistics of this CTA's columns, then the transposed tiles
-#pragma unroll 1
-  for (int q = 0; q < kStatTiles; ++q) {
-    const int tile = blockIdx.x + q * gridDim.x;
-    if (tile >= ntiles) break;
-    const int r0 = (tile / ct) * kStatTile, c0 = (tile % ct) * kStatTile;
-    float* t = st_smem + q * kStatTile * kStatPitch;
-    float* mus = reinterpret_cast<float*>(red);  // [2][128] floats: mu, scale
-    if (threadIdx.x < kStatTile) {
-      const int j = c0 + threadIdx.x + 1;
-      float mu = 0.f, sc = 1.f;
-      if (j <= m) {
-        double S1 = 0.0, S2 = 0.0;
-        for (int r = 0; r < rt; ++r) {
-          S1 += __ldcg(part + (size_t)r * m + (j - 1));
-          if constexpr (kCorr) S2 += __ldcg(part + (size_t)(rt + r) * m + (j - 1));
-        }
-        mu = (float)(S1 / (double)kFloatN);
-        float sd = 1.f;
-        if constexpr (kCorr) {
-          const double qq = S2 - 2.0 * (double)mu * S1 + (double)n * (double)mu * (double)mu;
-          const float sdv = (float)sqrt(fmax(qq, 0.0) / (double)kFloatN);
-          sd = sdv <= kEps ? 1.0f : sdv;
-          sc = sqrtf(kFloatN) * sd;
-        }
-        if (r0 == 0) {
-          mean[j] = mu;
-          if constexpr (kCorr) stdv[j] = sd;
-        }
-      }
-      mus[threadIdx.x] = mu;
-      mus[kStatTile + threadIdx.x] = sc;
-    }
-    __syncthreads();
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if constexpr (kF16) {
-      // warp w: columns w, w + 8, ...; lane: rows 2 lane + 64 e, +1 (one half2 each: 128-byte rows)
-      __half* xh = reinterpret_cast<__half*>(xt_);
-      __half* xl = reinterpret_cast<__half*>(xt_lo_);
-#pragma unroll 2
-      for (int cc = w; cc < kStatTile; cc += kStatThreads / 32) {
-        const int j = c0 + cc;
-        if (j >= m) break;
-        const float mu = mus[cc], sc = mus[kStatTile + cc];
-#pragma unroll
-        for (int e = 0; e < kStatTile / 64; ++e) {
-          const int r = 2 * lane + 64 * e, i = r0 + r;
-          if (i < n) {
-            float x0 = t[r * kStatPitch + cc] - mu, x1 = t[(r + 1) * kStatPitch + cc] - mu;
-            if constexpr (kCorr) {
-              x0 /= sc;
-              x1 /= sc;
-            }
-            __half2 hh, ll;
-            f16op::split1(x0, sc16, hh.x, ll.x);
-            f16op::split1(i + 1 < n ? x1 : 0.f, sc16, hh.y, ll.y);
-            *reinterpret_cast<__half2*>(xh + (size_t)j * ldx + i) = hh;  // ldx, i even: 4-byte aligned
-            *reinterpret_cast<__half2*>(xl + (size_t)j * ldx + i) = ll;
-          }
-        }
-      }
-    } else {
-      float* xt = reinterpret_cast<float*>(xt_);
-      float* xt_lo = reinterpret_cast<float*>(xt_lo_);
-      // warp w: columns w, w + 8, ...; lane: rows lane + 32 e (128-byte rows of Xt)
 #pragma unroll 4
-      for (int cc = w; cc < kStatTile; cc += kStatThreads / 32) {
-        const int j = c0 + cc;  // 0-based Xt row
-        if (j >= m) break;
-        const float mu = mus[cc], sc = mus[kStatTile + cc];
+    for (int i = g; i < n; i += 16) {
+      const float v = cs_smem[i * (kCS + 1) + c];
+      s1 += v;
+      if constexpr (kCorr) s2 += (double)v * v;
+    }
+    r1[g][c] = s1;
+    if constexpr (kCorr) r2[g][c] = s2;
+  }
+  __syncthreads();
+  if (t < kCS) {
+    double S1 = 0.0, S2 = 0.0;
 #pragma unroll
-        for (int e = 0; e < kStatTile / 32; ++e) {
-          const int r = lane + 32 * e, i = r0 + r;
-          if (i < n) {
-            float x = t[r * kStatPitch + cc] - mu;
-            if constexpr (kCorr) x /= sc;
-            xt[(size_t)j * ldx + i] = x;
-            xt_lo[(size_t)j * ldx + i] = x - tma::trunc_tf32(x);
-          }
-        }
+    for (int q = 0; q < 16; ++q) {
+      S1 += r1[q][t];
+      if constexpr (kCorr) S2 += r2[q][t];
+    }
+    const float mu = (float)(S1 / (double)kFloatN);
+    float sc = 1.f;
+    if (j0 + t + 1 <= m) {
+      mean[j0 + t + 1] = mu;
+      if constexpr (kCorr) {
+        const double qq = S2 - 2.0 * (double)mu * S1 + (double)n * (double)mu * (double)mu;
+        const float sdv = (float)sqrt(fmax(qq, 0.0) / (double)kFloatN);
+        const float sd = sdv <= kEps ? 1.0f : sdv;
+        stdv[j0 + t + 1] = sd;
+        sc = sqrtf(kFloatN) * sd;
       }
     }
-    __syncthreads();
+    mus[t] = mu;
+    scs[t] = sc;
+  }
+  __syncthreads();
+  // ---- centre (and scale) in place, per-column max|x'|
+  {
+    const float mu = mus[c], sc = scs[c];
+    float mx = 0.f;
+#pragma unroll 4
+    for (int i = g; i < n; i += 16) {
+      float x = cs_smem[i * (kCS + 1) + c] - mu;
+      if constexpr (kCorr) x /= sc;
+      cs_smem[i * (kCS + 1) + c] = x;
+      mx = fmaxf(mx, fabsf(x));
+    }
+    rmax[g][c] = mx;
+  }
+  __syncthreads();
+  if (t < kCS) {
+    float mx = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) mx = fmaxf(mx, rmax[q][t]);
+    const float s = f16op::scale_of(mx);
+    s16[t] = s;
+    if (j0 + t < m) rinv[j0 + t] = 1.f / s;
+  }
+  __syncthreads();
+  // ---- each column -> one operand row (warp w: columns w, w + 8; lane: rows 2 lane + 64 e, +1)
+  const int w = t >> 5, lane = t & 31;
+#pragma unroll 1
+  for (int cc = w; cc < kCS; cc += kCSThreads / 32) {
+    if (j0 + cc >= m) break;
+    const float s = s16[cc];
+    __half* hrow = xh + (size_t)(j0 + cc) * ldx;
+    __half* lrow = xl + (size_t)(j0 + cc) * ldx;
+#pragma unroll 4
+    for (int i = 2 * lane; i < n; i += 64) {
+      __half2 hh, ll;
+      f16op::split1(cs_smem[i * (kCS + 1) + cc], s, hh.x, ll.x);
+      f16op::split1(i + 1 < n ? cs_smem[(i + 1) * (kCS + 1) + cc] : 0.f, s, hh.y, ll.y);
+      *reinterpret_cast<__half2*>(hrow + i) = hh;  // ldx and i even: 4-byte aligned
+      *reinterpret_cast<__half2*>(lrow + i) = ll;
+    }
   }
 }
 
@@ -505,11 +455,8 @@ inline void run(Workspace& ws, cudaStream_t s) {
       const int mp = (m + 3) / 4 * 4, np = (n + 7) / 8 * 8;
       const size_t xs = (size_t)m * np, gs = (size_t)m * mp;
       const int gx = (int)cdiv(m, 256);
-      const int rt = (int)cdiv(n, kStatTile), ntiles = rt * (int)cdiv(m, kStatTile);
-      const size_t part_doubles = 2 * (size_t)rt * m;
       float* X = ws.ensure_scratch((2 * xs + gs) * sizeof(float) + 2 * (m + 1) * sizeof(double) + 64 * 4 +
-                                   gx * sizeof(unsigned) + part_doubles * sizeof(double) + 256 +
-                                   (ntiles + 64) * sizeof(float));
+                                   gx * sizeof(unsigned) + (m + 64) * sizeof(float) + 256);
       if (!X) {
         launch_failed("CORR/COVAR stage 2: scratch allocation failed");
         return;
@@ -518,43 +465,26 @@ inline void run(Workspace& ws, cudaStream_t s) {
       float* G = Xlo + xs;
       double* acc = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(G + gs) + 255) & ~uintptr_t(255));
       unsigned* arrivals = reinterpret_cast<unsigned*>(acc + 2 * (m + 1));
-      double* part = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(arrivals + gx) + 255) & ~uintptr_t(255));
-      float* f16_scale = reinterpret_cast<float*>(part + part_doubles);  // [2]
-      float* tmax = f16_scale + 64;                                      // [ntiles]
-      // one cooperative pass when every tile fits in the co-resident CTAs'
-      // shared memory (PF_CC_FUSED=0 forces the two-launch path, A/B runs);
-      // then the Gram runs on 3xFP16 images (PF_TC_F16=0: 3xTF32)
-      static const bool fused_ok = [] {
-        const char* e = std::getenv("PF_CC_FUSED");
-        return !(e && e[0] == '0');
-      }();
-      const int sms = device_sms();
-      int* flags = fused_ok ? ws.ensure_tile_flags(s) : nullptr;
-      const bool f16 = tc_f16_enabled() && m >= 256;
-      const void* coop = f16 ? (const void*)stats_centre_coop<Bn, V, kCorr, true>
-                             : (const void*)stats_centre_coop<Bn, V, kCorr, false>;
-      const bool fused = flags && occupancy(coop, kStatThreads, kStatSmem) >= 1 && ntiles <= kStatTiles * sms;
+      float* rinv = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(arrivals + gx) + 255) & ~uintptr_t(255));
+      // 3xFP16 Gram (PF_TC_F16=0: 3xTF32) when the column strips fit in
+      // shared memory: statistics, centring and the operand split in one
+      // launch (strip_stats_f16); else the two-launch fp32 preparation
+      const bool f16 = tc_f16_enabled() && m >= 256 && n <= kCSMaxRows;
       F16Operands f16ops;
-      if (fused) {
-        const int grid = std::min(ntiles, sms);
-        int epoch = ++ws.tile_epoch;
-        void* xh = X;
-        void* xl = f16 ? (void*)(reinterpret_cast<__half*>(X) + xs) : (void*)Xlo;
-        void* args[] = {(void*)&data, (void*)&part, (void*)&tmax, (void*)&flags, (void*)&epoch, (void*)&mean,
-                        (void*)&stdv, (void*)&xh, (void*)&xl, (void*)&f16_scale, (void*)&m, (void*)&n, (void*)&np};
-        if (cudaLaunchCooperativeKernel(coop, dim3(grid), dim3(kStatThreads), args, kStatSmem, s) != cudaSuccess) {
-          launch_failed("CORR/COVAR stage 2: cooperative statistics launch rejected");
-          return;
-        }
+      if (f16) {
+        __half* xh = reinterpret_cast<__half*>(X);
+        __half* xl = xh + xs;
+        set_smem_attr((const void*)strip_stats_f16<Bn, V, kCorr>, (int)strip_smem(n));
+        strip_stats_f16<Bn, V, kCorr><<<cdiv(m, kCS), kCSThreads, strip_smem(n), s>>>(data, mean, stdv, xh, xl,
+                                                                                     rinv, m, n, np);
         f16ops.hi[0] = f16ops.hi[1] = xh;
         f16ops.lo[0] = f16ops.lo[1] = xl;
         f16ops.hi[2] = f16ops.hi[3] = f16ops.lo[2] = f16ops.lo[3] = nullptr;
         f16ops.kp = np;
-        f16ops.scale = f16_scale;
-        f16ops.sb = 0;
+        f16ops.rinv = f16ops.cinv = rinv;
       } else {
         cudaMemsetAsync(acc, 0, 2 * (m + 1) * sizeof(double) + gx * sizeof(unsigned), s);
-        int splits = std::max(1, std::min((int)cdiv(sms * 4, gx), (n + 31) / 32));
+        int splits = std::max(1, std::min((int)cdiv(device_sms() * 4, gx), (n + 31) / 32));
         const int rps = (int)cdiv(n, splits);
         splits = (int)cdiv(n, rps);
         colstats_fused<Bn, V, kCorr><<<dim3(gx, splits), 256, 0, s>>>(data, acc, arrivals, mean, stdv, m, n, rps);
@@ -563,7 +493,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
       }
       // Xt Xt^T with K-major operands
       TcGemmArgs g{m, m, n, 1.f, 0.f, X, np, false, X, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
-      if (fused && f16) {
+      if (f16) {
         g.f16 = &f16ops;
       } else {
         g.Alo = Xlo;
@@ -598,9 +528,9 @@ inline void run(Workspace& ws, cudaStream_t s) {
 inline int64_t launches(bool corr, int stage, int64_t m, int64_t n) {
   if (stage == 0) return corr ? 4 : 3;
   const int64_t stats = corr ? 4 : 2;
-  if (stage == 2) {  // [stats + centre fused | stats, centre], Gram, scatter
-    const int64_t tiles = cdiv(m, kStatTile) * cdiv(n, kStatTile);
-    return (tiles <= kStatTiles * device_sms() ? 1 : 2) + tc_tma_launches(m, m, n, false, true, true) + 1;
+  if (stage == 2) {  // [strip statistics + split | stats, centre], Gram, scatter
+    const bool f16 = tc_f16_enabled() && m >= 256 && n <= kCSMaxRows;
+    return (f16 ? 1 : 2) + tc_tma_launches(m, m, n, false, true, true) + 1;
   }
   return stats + 1 + 1 + 1 + (corr ? 1 : 0);
 }

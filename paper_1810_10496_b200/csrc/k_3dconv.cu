@@ -281,14 +281,22 @@ __device__ __forceinline__ void load_rows(PlaneRows<R, KV>& P, const float* __re
   }
 }
 
+// Linear grid, i-chunk fastest: the CTAs of consecutive chunks of one (k, j)
+// column are launched together, so the two halo planes a chunk shares with
+// its neighbour are read from HBM once and hit L2 the second time (with the
+// chunk index slowest, neighbours ran far apart and inputs larger than L2
+// were read 10/8 times).
 template <BenchId Bn, int V, int R, int PD, int CH, int TX, int TY, int KV>
 __global__ void __launch_bounds__(TX * TY) conv3d_s2d(const float* __restrict__ A, float* __restrict__ B, int ni,
-                                                      int nj, int nk) {
+                                                      int nj, int nk, int nchunk, int nbx, int nbxy) {
   constexpr int W = 4 * KV;  // outputs along k per thread
-  const int kq = W * (blockIdx.x * TX + threadIdx.x);
-  const int jr = 1 + (blockIdx.y * TY + threadIdx.y) * R;
+  // nbxy > 0 (PF_C3_ZSLOW=1, A/B runs): the previous order, chunk slowest
+  const int chunk = nbxy ? blockIdx.x / nbxy : blockIdx.x % nchunk;
+  const int bxy = nbxy ? blockIdx.x % nbxy : blockIdx.x / nchunk;
+  const int kq = W * ((bxy % nbx) * TX + threadIdx.x);
+  const int jr = 1 + ((bxy / nbx) * TY + threadIdx.y) * R;
   if (kq >= nk || jr > nj - 2) return;
-  const int i0 = 1 + blockIdx.z * CH, i1 = min(ni - 1, i0 + CH);  // outputs [i0, i1), inputs i0-1 .. i1
+  const int i0 = 1 + chunk * CH, i1 = min(ni - 1, i0 + CH);  // outputs [i0, i1), inputs i0-1 .. i1
   const int plane = nj * nk;                                      // < 2^31 (checked on the host)
   int roff[R + 2];
 #pragma unroll
@@ -355,8 +363,13 @@ void launch_s2d(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s
       return;
     }
   }
-  conv3d_s2d<B_3DCONV, V, R, PD, CH, TX, TY, KV><<<dim3(cdiv(nk, 4 * KV * TX), cdiv(nj - 2, TY * R), cdiv(ni - 2, CH)),
-                                                   dim3(TX, TY), 0, s>>>(A, B, ni, nj, nk);
+  static const bool zslow = [] {
+    const char* e = std::getenv("PF_C3_ZSLOW");
+    return e && e[0] == '1';
+  }();
+  const int nbx = (int)cdiv(nk, 4 * KV * TX), nby = (int)cdiv(nj - 2, TY * R), nchunk = (int)cdiv(ni - 2, CH);
+  conv3d_s2d<B_3DCONV, V, R, PD, CH, TX, TY, KV><<<(unsigned)nbx * nby * nchunk, dim3(TX, TY), 0, s>>>(
+      A, B, ni, nj, nk, nchunk, nbx, zslow ? nbx * nby : 0);
 }
 
 // PF_C3=t (A/B runs) selects the TMA plane-streaming kernel (38.9 us at 256^3,

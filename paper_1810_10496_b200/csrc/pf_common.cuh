@@ -117,35 +117,7 @@ struct Workspace {
   float* ensure_aux(size_t bytes);  // defined in abi.cu
 };
 constexpr int kTileFlags = 4096;
-// [0, kTileFlagsGemm): split-K tile flags; the last ints are self-resetting
-// counters: the grid barrier (arrival counter, release flag) of persistent
-// cooperative kernels and the 3xFP16 absmax arrival counter
-constexpr int kTileFlagsGemm = kTileFlags - 8;
-constexpr int kGridBarCounter = kTileFlags - 2, kGridBarFlag = kTileFlags - 1;
-constexpr int kF16Counter = kTileFlags - 3;  // arrival counter of the 3xFP16 operand absmax
-
-// Grid-wide barrier for a cooperatively launched (all CTAs co-resident)
-// kernel: the last arrival resets the counter and releases the epoch, so no
-// per-launch memset is needed.  Called by all threads of the CTA.
-__device__ __forceinline__ void grid_barrier(int* flags, int epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-    unsigned* ctr = reinterpret_cast<unsigned*>(flags + kGridBarCounter);
-    if (atomicAdd(ctr, 1u) == total - 1) {
-      atomicExch(ctr, 0u);
-      __threadfence();
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + kGridBarFlag), "r"(epoch) : "memory");
-    } else {
-      int v;
-      do {
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + kGridBarFlag) : "memory");
-      } while (v != epoch);
-    }
-  }
-  __syncthreads();
-}
+constexpr int kTileFlagsGemm = kTileFlags;  // split-K tile flags
 
 // Graph-staged variants: capture `body` once per (workspace, key) and return
 // the executable graph (abi.cu).  Launch with cudaGraphLaunch(exec, stream).

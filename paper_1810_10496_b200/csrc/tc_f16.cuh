@@ -5,20 +5,21 @@
 // split that holds fp32 tolerance costs half the tensor-core time and half the
 // operand traffic.
 //
-// Split: s = 2^e per operand group with max|x| * s in [2^14, 2^15), then
+// Split, per operand ROW (a row of op(A) or of op(B)^T: one output row /
+// column): s = 2^e with max|x_row| s in [2^14, 2^15), then
 //   hi = fp16_rn(x s),  lo = fp16_rn(x s - hi)
 // x s is exact (power of two), |x s - hi| <= 2^-11 |x s|, and lo carries
 // the next 11 bits, so hi + lo = x s to 2^-22 relative -- the same 22
 // operand bits as 3xTF32 (whose lo is truncated to TF32 by the tensor core).
-// Elements below 2^-17 max|x| lose low bits of lo to fp16 subnormals; their
-// absolute error stays below 2^-40 max|x|.  The product is accumulated as
-// lo*hi + hi*lo + hi*hi in the fp32 TMEM accumulator and the epilogue
-// multiplies alpha by 1 / (sA sB) (exact).
-//
-// Launches per contraction: f16_absmax (every operand, one arrival counter,
-// the last block turns the maxima into the scales) and f16_split (every
-// distinct operand: K-major rows converted in place order, MN-major operands
-// transposed through shared memory into K-major images).
+// Elements below 2^-17 of their row's max lose low bits of lo to fp16
+// subnormals; their absolute error stays below 2^-40 of the row max.  The
+// product accumulates lo*hi + hi*lo + hi*hi in the fp32 TMEM accumulator and
+// the epilogue multiplies by alpha / (s_row s_col), exactly (powers of two).
+// Per-row scales need no global reduction: every row is scaled by the warp
+// (K-major) or CTA (MN-major strip) that converts it -- one launch for all
+// operands of a contraction.  K-concatenated products (SYR2K: A B^T + B A^T)
+// share one scale per row index across both arrays, so both pairs carry the
+// same s_i s_j.
 #pragma once
 #include "pf_common.cuh"
 #include "tc_gemm.cuh"
@@ -26,41 +27,45 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace pf {
 namespace f16op {
 
 constexpr int kMaxOps = 4;
+constexpr int kStrip = 16;  // MN-major operands: columns per CTA
 
 struct Op {
-  const float* x;  // storage: mn ? K rows x R cols : R rows x K cols, pitch ld (floats)
+  const float* x;   // storage: mn ? K rows x R cols : R rows x K cols, pitch ld (floats)
+  const float* x2;  // K-major only: second array sharing the row scales (K-concatenated pair), or nullptr
   int mn;
   int R, K, ld;
-  __half* hi;      // image: R rows x K halfs, pitch kp
+  __half* hi;       // image: R rows x K halfs, pitch kp
   __half* lo;
-  int grp;         // scale group (0 or 1)
+  __half* hi2;      // image of x2
+  __half* lo2;
+  float* rinv;      // [R] 1 / s_row
 };
 
 struct Ops {
   Op op[kMaxOps];
   int n;
   int kp;
-  float* partial;  // [n][gridDim.x] block maxima
-  unsigned* counter;
-  float* scale;    // [2]
 };
 
-__device__ __forceinline__ float block_max(float v, float* red) {
+__device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+  v = warp_max(v);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) red[w] = v;
   __syncthreads();
-  if (w == 0) {
-    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  }
+  if (w == 0) v = warp_max(lane < (int)(blockDim.x >> 5) ? red[lane] : 0.f);
   return v;  // valid in warp 0
 }
 
@@ -72,127 +77,168 @@ __device__ __forceinline__ float scale_of(float amax) {
   return ldexpf(1.f, 15 - ex);
 }
 
-// blockIdx.y = operand; grid-stride over its storage rectangle
-template <BenchId Bn, int V>
-__global__ void __launch_bounds__(256) f16_absmax(const Ops ops) {
-  __shared__ float red[8];
-  __shared__ bool last;
-  const Op& o = ops.op[blockIdx.y];
-  const int rows = o.mn ? o.K : o.R, cols = o.mn ? o.R : o.K;
-  float m = 0.f;
-  const bool vec = (o.ld % 4 == 0) && (cols % 4 == 0) && (reinterpret_cast<uintptr_t>(o.x) % 16 == 0);
-  if (vec) {
-    const int c4 = cols / 4;
-    const int64_t n4 = (int64_t)rows * c4;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t r = i / c4, c = i % c4;
-      const float4 v = __ldg(reinterpret_cast<const float4*>(o.x + r * o.ld) + c);
-      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-    }
-  } else {
-    const int64_t n = (int64_t)rows * cols;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-      m = fmaxf(m, fabsf(__ldg(o.x + (i / cols) * o.ld + i % cols)));
-  }
-  m = block_max(m, red);
-  if (threadIdx.x == 0) {
-    ops.partial[blockIdx.y * gridDim.x + blockIdx.x] = m;
-    __threadfence();
-    last = atomicAdd(ops.counter, 1u) == gridDim.x * gridDim.y - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // last block: per-group maxima -> scales; reset the counter for the next launch
-  if (threadIdx.x < 32) {
-    float g[2] = {0.f, 0.f};
-    for (int j = 0; j < ops.n; ++j)
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
-        const float v = __ldcg(ops.partial + j * gridDim.x + b);
-        if (ops.op[j].grp) g[1] = fmaxf(g[1], v); else g[0] = fmaxf(g[0], v);
-      }
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int s = 16; s > 0; s >>= 1) g[q] = fmaxf(g[q], __shfl_xor_sync(0xffffffffu, g[q], s));
-    if (threadIdx.x == 0) {
-      ops.scale[0] = scale_of(g[0]);
-      ops.scale[1] = scale_of(g[1]);
-      atomicExch(ops.counter, 0u);
-    }
-  }
-}
-
 __device__ __forceinline__ void split1(float x, float s, __half& h, __half& l) {
   const float y = x * s;
   h = __float2half_rn(y);
   l = __float2half_rn(y - __half2float(h));
 }
 
-// blockIdx.y = operand.  K-major: each warp converts rows, 4 floats per lane
-// per step.  MN-major: 64 (k) x 64 (r) tiles transposed through shared memory.
-template <BenchId Bn, int V>
-__global__ void __launch_bounds__(256) f16_split(const Ops ops) {
-  __shared__ float t[64][65];
-  const Op& o = ops.op[blockIdx.y];
-  if (!o.hi) return;  // duplicate operand: its image is written by an earlier slot
-  const float s = __ldcg(ops.scale + o.grp);
-  const int kp = ops.kp;
-  if (!o.mn) {
-    const bool vec = (o.ld % 4 == 0) && (o.K % 4 == 0) && (reinterpret_cast<uintptr_t>(o.x) % 16 == 0);
-    const int warps = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = blockIdx.x * warps + w; r < o.R; r += gridDim.x * warps) {
-      const float* row = o.x + (size_t)r * o.ld;
-      __half* hrow = o.hi + (size_t)r * kp;
-      __half* lrow = o.lo + (size_t)r * kp;
-      if (vec) {
-        for (int k = 4 * lane; k < o.K; k += 128) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(row + k));
-          __half h[4], l[4];
-          split1(v.x, s, h[0], l[0]);
-          split1(v.y, s, h[1], l[1]);
-          split1(v.z, s, h[2], l[2]);
-          split1(v.w, s, h[3], l[3]);
-          *reinterpret_cast<uint2*>(hrow + k) = *reinterpret_cast<const uint2*>(h);
-          *reinterpret_cast<uint2*>(lrow + k) = *reinterpret_cast<const uint2*>(l);
-        }
-      } else {
-        for (int k = lane; k < o.K; k += 32) split1(__ldg(row + k), s, hrow[k], lrow[k]);
+__device__ __forceinline__ float amax4(float4 v) {
+  return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+
+__device__ __forceinline__ void store4(__half* hi, __half* lo, float4 v, float s) {
+  __half h[4], l[4];
+  split1(v.x, s, h[0], l[0]);
+  split1(v.y, s, h[1], l[1]);
+  split1(v.z, s, h[2], l[2]);
+  split1(v.w, s, h[3], l[3]);
+  *reinterpret_cast<uint2*>(hi) = *reinterpret_cast<const uint2*>(h);
+  *reinterpret_cast<uint2*>(lo) = *reinterpret_cast<const uint2*>(l);
+}
+
+// K-major row r of op (and of x2): warp-cooperative; rows of up to 2048
+// floats stay in registers between the max and the conversion.
+template <bool kDual>
+__device__ __forceinline__ void split_row(const Op& o, int kp, int r, int lane) {
+  constexpr int kRegF4 = 16;  // 16 float4 per lane: K <= 2048
+  const float* row = o.x + (size_t)r * o.ld;
+  const float* row2 = kDual ? o.x2 + (size_t)r * o.ld : nullptr;
+  const bool vec = (o.ld % 4 == 0) && (o.K % 4 == 0) && (reinterpret_cast<uintptr_t>(o.x) % 16 == 0) &&
+                   (!o.x2 || reinterpret_cast<uintptr_t>(o.x2) % 16 == 0);
+  float m = 0.f;
+  if (vec && o.K <= 128 * kRegF4) {
+    float4 v[kRegF4], v2[kRegF4];
+#pragma unroll
+    for (int u = 0; u < kRegF4; ++u) {
+      const int k = 4 * lane + 128 * u;
+      v[u] = k < o.K ? __ldg(reinterpret_cast<const float4*>(row + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v2[u] = (row2 && k < o.K) ? __ldg(reinterpret_cast<const float4*>(row2 + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kRegF4; ++u) m = fmaxf(m, fmaxf(amax4(v[u]), amax4(v2[u])));
+    const float s = scale_of(warp_max(m));
+    if (lane == 0) o.rinv[r] = 1.f / s;
+#pragma unroll
+    for (int u = 0; u < kRegF4; ++u) {
+      const int k = 4 * lane + 128 * u;
+      if (k < o.K) {
+        store4(o.hi + (size_t)r * kp + k, o.lo + (size_t)r * kp + k, v[u], s);
+        if (row2) store4(o.hi2 + (size_t)r * kp + k, o.lo2 + (size_t)r * kp + k, v2[u], s);
       }
     }
     return;
   }
-  // MN-major storage X[k][r] -> image[r][k]
-  const int tk = (o.K + 63) / 64, tr = (o.R + 63) / 64;
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
-  for (int tile = blockIdx.x; tile < tk * tr; tile += gridDim.x) {
-    const int k0 = (tile / tr) * 64, r0 = (tile % tr) * 64;
+  // long or unaligned rows: max pass, then a conversion pass (re-read from L1/L2)
+  for (int k = lane; k < o.K; k += 32) {
+    m = fmaxf(m, fabsf(__ldg(row + k)));
+    if (row2) m = fmaxf(m, fabsf(__ldg(row2 + k)));
+  }
+  const float s = scale_of(warp_max(m));
+  if (lane == 0) o.rinv[r] = 1.f / s;
+  for (int k = lane; k < o.K; k += 32) {
+    split1(__ldg(row + k), s, o.hi[(size_t)r * kp + k], o.lo[(size_t)r * kp + k]);
+    if (row2) split1(__ldg(row2 + k), s, o.hi2[(size_t)r * kp + k], o.lo2[(size_t)r * kp + k]);
+  }
+}
+
+// MN-major strip: storage X[k][r], columns r0 .. r0+15 -> image rows r0 ..
+// r0+15 (K halfs each).  K <= kStripMaxK: the whole K x 16 strip lands in
+// shared memory through cp.async (every 4-byte load in flight at once),
+// per-column max, then each column leaves as one image row (warp w: rows w,
+// w + 8; lane: halfs 2 lane + 64 e, +1 -- 128-byte stores).  Longer K:
+// streamed twice (max pass, then 64-deep blocks transposed through shared
+// memory).
+constexpr int kStripMaxK = 2944;  // K * 17 * 4 bytes <= 200 KB
+inline size_t strip_smem_bytes(int K) { return (size_t)K * (kStrip + 1) * sizeof(float); }
+
+__device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* strip) {
+  __shared__ float red[16][kStrip + 1];
+  __shared__ float sc[kStrip];
+  const int t = threadIdx.x, c = t % kStrip, g = t / kStrip;  // 16 x 16
+  const int r = r0 + c;
+  float m = 0.f;
+  if (o.K <= kStripMaxK) {
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(strip));
+    for (int k = g; k < o.K; k += 16) {
+      if (r < o.R)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sbase + 4u * (uint32_t)(k * (kStrip + 1) + c)),
+                     "l"(o.x + (size_t)k * o.ld + r)
+                     : "memory");
+      else
+        strip[k * (kStrip + 1) + c] = 0.f;
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+    __syncthreads();
 #pragma unroll 4
-    for (int q = ty; q < 64; q += 4) {
-      const int k = k0 + q, r = r0 + tx;
-      t[q][tx] = (k < o.K && r < o.R) ? __ldg(o.x + (size_t)k * o.ld + r) : 0.f;
+    for (int k = g; k < o.K; k += 16) m = fmaxf(m, fabsf(strip[k * (kStrip + 1) + c]));
+  } else if (r < o.R) {
+#pragma unroll 8
+    for (int k = g; k < o.K; k += 16) m = fmaxf(m, fabsf(__ldg(o.x + (size_t)k * o.ld + r)));
+  }
+  red[g][c] = m;
+  __syncthreads();
+  if (t < kStrip) {
+    float mm = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) mm = fmaxf(mm, red[q][t]);
+    const float s = scale_of(mm);
+    sc[t] = s;
+    if (r0 + t < o.R) o.rinv[r0 + t] = 1.f / s;
+  }
+  __syncthreads();
+  if (o.K <= kStripMaxK) {
+    const int w = t >> 5, lane = t & 31;
+#pragma unroll 1
+    for (int cc = w; cc < kStrip; cc += 8) {
+      if (r0 + cc >= o.R) break;
+      const float s = sc[cc];
+      __half* hrow = o.hi + (size_t)(r0 + cc) * kp;
+      __half* lrow = o.lo + (size_t)(r0 + cc) * kp;
+#pragma unroll 4
+      for (int k = 2 * lane; k < o.K; k += 64) {
+        __half2 hh, ll;
+        split1(strip[k * (kStrip + 1) + cc], s, hh.x, ll.x);
+        split1(k + 1 < o.K ? strip[(k + 1) * (kStrip + 1) + cc] : 0.f, s, hh.y, ll.y);
+        *reinterpret_cast<__half2*>(hrow + k) = hh;  // kp and k even: 4-byte aligned
+        *reinterpret_cast<__half2*>(lrow + k) = ll;
+      }
+    }
+    __syncthreads();  // the strip buffer is reused by the next strip
+    return;
+  }
+  __shared__ __align__(16) __half th[kStrip][64 + 8], tl[kStrip][64 + 8];
+  const float s = sc[c];
+  for (int k0 = 0; k0 < o.K; k0 += 64) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int kk = g + 16 * u, k = k0 + kk;
+      const float v = (r < o.R && k < o.K) ? __ldg(o.x + (size_t)k * o.ld + r) : 0.f;
+      split1(v, s, th[c][kk], tl[c][kk]);
     }
     __syncthreads();
-    // thread: image row r0 + q, halfs k0 + 2 tx2, +1 (32 lanes x 4 bytes = 128 B per row)
-    const int tx2 = threadIdx.x & 31, ty2 = threadIdx.x >> 5;  // 32 x 8
-#pragma unroll 2
-    for (int q = ty2; q < 64; q += 8) {
-      const int r = r0 + q, k = k0 + 2 * tx2;
-      if (r < o.R && k < o.K) {
-        __half2 h, l;
-        split1(t[2 * tx2][q], s, h.x, l.x);
-        if (k + 1 < o.K) {
-          split1(t[2 * tx2 + 1][q], s, h.y, l.y);
-          *reinterpret_cast<__half2*>(o.hi + (size_t)r * kp + k) = h;
-          *reinterpret_cast<__half2*>(o.lo + (size_t)r * kp + k) = l;
-        } else {
-          o.hi[(size_t)r * kp + k] = h.x;
-          o.lo[(size_t)r * kp + k] = l.x;
-        }
-      }
+    // 16 image rows x 64 halfs (128 B) per array: thread -> row t / 16, halfs 4 (t % 16) .. +3
+    const int rr = t / 16, q = t % 16, k = k0 + 4 * q;
+    if (r0 + rr < o.R && k < o.K && k + 4 <= kp) {
+      *reinterpret_cast<uint2*>(o.hi + (size_t)(r0 + rr) * kp + k) = *reinterpret_cast<const uint2*>(&th[rr][4 * q]);
+      *reinterpret_cast<uint2*>(o.lo + (size_t)(r0 + rr) * kp + k) = *reinterpret_cast<const uint2*>(&tl[rr][4 * q]);
     }
     __syncthreads();
   }
+}
+
+// blockIdx.y = operand.  K-major operands: one warp per row (8 rows per
+// CTA); MN-major operands: one 16-column strip per CTA.
+template <BenchId Bn, int V, bool kDual>
+__global__ void __launch_bounds__(256) f16_split(const Ops ops) {
+  extern __shared__ float f16_strip[];  // MN-major strips (dynamic; none when every operand is K-major)
+  const Op& o = ops.op[blockIdx.y];
+  if (o.mn) {
+    for (int r0 = blockIdx.x * kStrip; r0 < o.R; r0 += gridDim.x * kStrip) split_strip(o, ops.kp, r0, f16_strip);
+    return;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * 8 + w; r < o.R; r += gridDim.x * 8) split_row<kDual>(o, ops.kp, r, lane);
 }
 
 }  // namespace f16op
@@ -207,66 +253,79 @@ inline bool tc_f16_enabled() {
   return on;
 }
 
-// Prepares the 3xFP16 images of a contraction's operands (two launches) in
-// the workspace scratch and describes them in `out`.  Distinct operand
-// arrays get one image each (SYRK's A serves both sides).  One scale group
-// for K-concatenated products (both pairs must share sA sB), else A and B
-// are scaled independently.
+// Prepares the 3xFP16 images and per-row inverse scales of a contraction's
+// operands in the workspace scratch (ONE launch) and describes them in
+// `out`.  Distinct operand arrays get one image each (SYRK's A serves both
+// sides); a K-concatenated product (A2, B2 = B, A: SYR2K) converts A and B
+// as one paired operand with shared row scales.
 template <BenchId Bn, int V>
 inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cudaStream_t s) {
   const bool dual = a.A2 != nullptr;
-  const int nops = dual ? 4 : 2;
-  const float* ptr[4] = {a.A, a.B, a.A2, a.B2};
-  const int mn[4] = {a.ta ? 1 : 0, a.tb ? 0 : 1, a.ta ? 1 : 0, a.tb ? 0 : 1};
-  const int R[4] = {a.M, a.N, a.M, a.N};
-  const int ld[4] = {a.lda, a.ldb, a.lda, a.ldb};
+  if (dual && !(a.A2 == a.B && a.B2 == a.A && !a.ta && a.tb && a.M == a.N && a.lda == a.ldb))
+    return false;  // only the symmetric K-concatenation (A B^T + B A^T) shares row scales
   const int kp = (a.K + 7) / 8 * 8;
-  int img[4], nimg = 0, first[4];
-  for (int i = 0; i < nops; ++i) {
-    img[i] = -1;
-    for (int j = 0; j < i; ++j)
-      if (ptr[j] == ptr[i] && mn[j] == mn[i] && R[j] == R[i] && ld[j] == ld[i]) img[i] = img[j];
-    if (img[i] < 0) {
-      first[nimg] = i;
-      img[i] = nimg++;
-    }
-  }
-  int* flags = ws.ensure_tile_flags(s);
-  if (!flags) return false;
-  const int G = 2 * device_sms();
-  const size_t per = ((size_t)std::max(a.M, a.N) * kp * 2 + 255) / 256 * 256;
-  uint8_t* base = reinterpret_cast<uint8_t*>(ws.ensure_scratch(2 * nimg * per + (size_t)nimg * G * 4 + 256));
+  const size_t img = ((size_t)std::max(a.M, a.N) * kp * 2 + 255) / 256 * 256;
+  const size_t vec = ((size_t)std::max(a.M, a.N) + 64) * sizeof(float);  // inverse scales (padded)
+  const bool same = !dual && a.A == a.B && a.ta == !a.tb && a.M == a.N && a.lda == a.ldb;  // SYRK: A A^T
+  const int nimg = dual ? 2 : (same ? 1 : 2);
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws.ensure_scratch(2 * nimg * img + 2 * vec + 256));
   if (!base) return false;
+  auto H = [&](int i) { return reinterpret_cast<__half*>(base + i * img); };
+  float* rinv_a = reinterpret_cast<float*>(base + 2 * nimg * img);
+  float* rinv_b = reinterpret_cast<float*>(base + 2 * nimg * img + vec);
   f16op::Ops ops;
   std::memset(&ops, 0, sizeof(ops));
-  ops.n = nimg;
   ops.kp = kp;
-  ops.partial = reinterpret_cast<float*>(base + 2 * nimg * per);
-  ops.scale = ops.partial + (size_t)nimg * G;
-  ops.counter = reinterpret_cast<unsigned*>(flags + kF16Counter);
-  const bool b_own = !dual && img[1] != img[0];
-  for (int q = 0; q < nimg; ++q) {
-    const int i = first[q];
-    f16op::Op& o = ops.op[q];
-    o.x = ptr[i];
-    o.mn = mn[i];
-    o.R = R[i];
+  if (dual) {  // one paired K-major operand: rows of A and B, shared scales
+    f16op::Op& o = ops.op[0];
+    o.x = a.A;
+    o.x2 = a.B;
+    o.mn = 0;
+    o.R = a.M;
     o.K = a.K;
-    o.ld = ld[i];
-    o.hi = reinterpret_cast<__half*>(base + 2 * q * per);
-    o.lo = reinterpret_cast<__half*>(base + (2 * q + 1) * per);
-    o.grp = (b_own && i == 1) ? 1 : 0;
+    o.ld = a.lda;
+    o.hi = H(0), o.lo = H(1), o.hi2 = H(2), o.lo2 = H(3);
+    o.rinv = rinv_a;
+    ops.n = 1;
+    out.hi[0] = H(0), out.lo[0] = H(1);  // op(A)  = A
+    out.hi[1] = H(2), out.lo[1] = H(3);  // op(B)  = B
+    out.hi[2] = H(2), out.lo[2] = H(3);  // op(A2) = B
+    out.hi[3] = H(0), out.lo[3] = H(1);  // op(B2) = A
+    out.rinv = rinv_a;
+    out.cinv = rinv_a;
+  } else {
+    f16op::Op& oa = ops.op[0];
+    oa.x = a.A, oa.mn = a.ta ? 1 : 0, oa.R = a.M, oa.K = a.K, oa.ld = a.lda;
+    oa.hi = H(0), oa.lo = H(1), oa.rinv = rinv_a;
+    ops.n = 1;
+    out.hi[0] = H(0), out.lo[0] = H(1);
+    out.rinv = rinv_a;
+    if (same) {
+      out.hi[1] = H(0), out.lo[1] = H(1);
+      out.cinv = rinv_a;
+    } else {
+      f16op::Op& ob = ops.op[1];
+      ob.x = a.B, ob.mn = a.tb ? 0 : 1, ob.R = a.N, ob.K = a.K, ob.ld = a.ldb;
+      ob.hi = H(2), ob.lo = H(3), ob.rinv = rinv_b;
+      ops.n = 2;
+      out.hi[1] = H(2), out.lo[1] = H(3);
+      out.cinv = rinv_b;
+    }
+    out.hi[2] = out.hi[3] = out.lo[2] = out.lo[3] = nullptr;
   }
-  for (int i = 0; i < nops; ++i) {
-    out.hi[i] = ops.op[img[i]].hi;
-    out.lo[i] = ops.op[img[i]].lo;
-  }
-  for (int i = nops; i < 4; ++i) out.hi[i] = out.lo[i] = nullptr;
   out.kp = kp;
-  out.scale = ops.scale;
-  out.sb = b_own ? 1 : 0;
-  f16op::f16_absmax<Bn, V><<<dim3(G, nimg), 256, 0, s>>>(ops);
-  f16op::f16_split<Bn, V><<<dim3(G, nimg), 256, 0, s>>>(ops);
+  const int rows = std::max(a.M, a.N);
+  const int grid = std::max((rows + 7) / 8, (rows + f16op::kStrip - 1) / f16op::kStrip);
+  const dim3 g3(std::min(grid, 8 * device_sms()), ops.n);
+  bool any_mn = false;
+  for (int i = 0; i < ops.n; ++i) any_mn |= ops.op[i].mn != 0;
+  const size_t smem = any_mn && a.K <= f16op::kStripMaxK ? f16op::strip_smem_bytes(a.K) : 0;
+  if (dual) {
+    f16op::f16_split<Bn, V, true><<<g3, 256, 0, s>>>(ops);
+  } else {
+    set_smem_attr((const void*)f16op::f16_split<Bn, V, false>, (int)smem);
+    f16op::f16_split<Bn, V, false><<<g3, 256, smem, s>>>(ops);
+  }
   return true;
 }
 

@@ -30,14 +30,14 @@
 namespace pf {
 
 // 3xFP16 operands (tc_f16.cuh): x * s = hi + lo with hi = fp16_rn(x s),
-// lo = fp16_rn(x s - hi), s a power of two per operand group putting
-// max|x s| in [2^14, 2^15); images are K-major R x kp halfs.
+// lo = fp16_rn(x s - hi), s a power of two per operand row putting
+// max|x_row s| in [2^14, 2^15); images are K-major R x kp halfs.
 struct F16Operands {
   const void* hi[4];   // op(A), op(B), op(A2), op(B2)
   const void* lo[4];
   int kp;              // image pitch (halfs, multiple of 8)
-  const float* scale;  // device [2]: scale of A's group, of B's group
-  int sb;              // index of B's scale (0: one scale for all operands)
+  const float* rinv;   // device [M (+pad)]: 1 / s of each row of op(A)   (output rows)
+  const float* cinv;   // device [N (+pad)]: 1 / s of each row of op(B)^T (output columns)
 };
 
 struct TcGemmArgs {

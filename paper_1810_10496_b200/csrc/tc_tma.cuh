@@ -72,8 +72,8 @@ struct TmaParams {
   uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides / k-step advance (bytes)
   int idesc_override;                 // probe only: -1 auto, else (a_major | b_major << 1)
   int f16;                            // operands are 3xFP16 images (hi/lo fp16, K-major): kind::f16 MMAs
-  const float* f16_scale;             // f16: power-of-two operand scales [A group, B group]; alpha / (sA sB)
-  int f16_sb;                         // f16: index of B's scale in f16_scale
+  const float* f16_rinv;              // f16: 1 / row scale per output row (power of two)
+  const float* f16_cinv;              // f16: 1 / row scale of op(B)^T per output column (padded to +64)
   int diag;                           // diagnostics only (PF_TC_DIAG): 1 skip lo split, 2 skip MMAs, 4 skip loads, 8 skip epilogue, 16 lane-row epilogue, 32 smem-transpose epilogue
 };
 
@@ -129,11 +129,7 @@ __device__ __forceinline__ uint32_t idesc(int m, int n, int a_mn, int b_mn, bool
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-// Effective alpha of the epilogue: 3xFP16 operands were scaled by powers of
-// two, undone here exactly.
-__device__ __forceinline__ float eff_alpha(const TmaParams& p) {
-  return p.f16 ? p.alpha / (__ldg(p.f16_scale) * __ldg(p.f16_scale + p.f16_sb)) : p.alpha;
-}
+
 
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
@@ -201,6 +197,8 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, float alpha, ui
   const bool want_mirror = mirror && split && lobuf != nullptr;  // same ring: transposed chunks
   const uint32_t sbuf = tc::smem_u32(buf);
   const uint32_t slo = (want_lo || want_mirror) ? tc::smem_u32(lobuf) : 0u;
+  // 3xFP16: undo the power-of-two row scales exactly (alpha / s_row, then / s_col)
+  const float ar = p.f16 ? alpha * __ldg(p.f16_rinv + min(row0 + lane, p.M - 1)) : alpha;
   if (use_c && lane == 0) {
     tc::mbar_expect_tx(bar, (uint32_t)nch * 4096u);
     for (int c = 0; c < nch; ++c) load_2d(sbuf + c * 4096, &p.tc, col0 + c * 32, row0, bar);
@@ -214,8 +212,12 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, float alpha, ui
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float4* slot = row + (j ^ (lane & 7));
-      float4 v = make_float4(alpha * __uint_as_float(r[4 * j]), alpha * __uint_as_float(r[4 * j + 1]),
-                             alpha * __uint_as_float(r[4 * j + 2]), alpha * __uint_as_float(r[4 * j + 3]));
+      float4 v = make_float4(ar * __uint_as_float(r[4 * j]), ar * __uint_as_float(r[4 * j + 1]),
+                             ar * __uint_as_float(r[4 * j + 2]), ar * __uint_as_float(r[4 * j + 3]));
+      if (p.f16) {
+        const float4 cs = __ldg(reinterpret_cast<const float4*>(p.f16_cinv + col0 + c * 32 + 4 * j));
+        v = make_float4(v.x * cs.x, v.y * cs.y, v.z * cs.z, v.w * cs.w);
+      }
       if (use_c) {
         const float4 ci = *slot;
         v = make_float4(fmaf(p.beta, ci.x, v.x), fmaf(p.beta, ci.y, v.y), fmaf(p.beta, ci.z, v.z),
@@ -432,17 +434,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
-      tma::epilogue_tma(p, tma::eff_alpha(p), tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
+      tma::epilogue_tma(p, p.alpha, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
                         p.sym && nb != mb);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
-      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
+      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                              p.Cin, p.ldc, p.D, p.ldd, split, lane);
     else if (!(p.diag & 8))
-      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
+      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                           p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
   }
   tc::fence_before();
@@ -661,17 +663,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
-      tma::epilogue_tma(p, tma::eff_alpha(p), tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
+      tma::epilogue_tma(p, p.alpha, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
                         p.sym && nb != mb);
       if (ordered && blockIdx.z == 0) tma::split_publish(p, warp, lane);
     }
     else if (p.diag & 16)
-      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
+      tc::epilogue_lane_rows(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                              p.Cin, p.ldc, p.D, p.ldd, split, lane);
     else if (!(p.diag & 8))
-      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, tma::eff_alpha(p), p.beta,
+      tc::epilogue_rows32(tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0, p.M, p.N, p.alpha, p.beta,
                           p.Cin, p.ldc, p.D, p.ldd, split, reinterpret_cast<float*>(smem) + quad * 32 * 33, lane);
   }
   tc::fence_before();
@@ -817,8 +819,8 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
     // 3xFP16: K-major fp16 hi / lo images for every operand (tc_f16.cuh)
     const F16Operands& f = *a.f16;
     p.f16 = 1;
-    p.f16_scale = f.scale;
-    p.f16_sb = f.sb;
+    p.f16_rinv = f.rinv;
+    p.f16_cinv = f.cinv;
     p.presplit = 1;
     if (!tma::operand_map_f16(&p.ta, f.hi[0], a.M, a.K, f.kp) || !tma::operand_map_f16(&p.tal, f.lo[0], a.M, a.K, f.kp) ||
         !tma::operand_map_f16(&p.tb, f.hi[1], a.N, a.K, f.kp) || !tma::operand_map_f16(&p.tbl, f.lo[1], a.N, a.K, f.kp))
@@ -866,6 +868,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
                  tma::make_map(&p.tc, a.Cin, a.N, a.M, a.ldc, 32, 32, false))
                     ? 1
                     : 0;
+  if (a.f16 && !p.tma_epi) return false;  // the row-scale epilogue is the TMA one
   const int kb1 = a.f16 ? (a.K + 63) / 64 : (a.K + 31) / 32;  // 128-byte k blocks
   const int kblocks = a.A2 ? 2 * kb1 : kb1;
   // split-K problems: beta pre-pass + TMA add-reductions, or the ordered

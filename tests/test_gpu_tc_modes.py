@@ -69,6 +69,7 @@ def test_syrk_wide_range(n, m):
     A = _wide(rng, (n, m))
     C = _wide(rng, (n, n), decades=2)
     (out,) = _run("SYRK", (n, m), {0: A, 1: C})
+    out = out.reshape(n, n)
     a64 = A.astype(np.float64)
     ref = 12435.0 * (a64 @ a64.T) + 4546.0 * C.astype(np.float64)
     _check(out, ref)
@@ -80,7 +81,7 @@ def test_2mm_wide_range_f16_path():
     A = _wide(rng, (n, n), 6)
     B = _wide(rng, (n, n), 6)
     D = _wide(rng, (n, n), 4)
-    outs = _run("2MM", (n, n, n, n), {0: A, 1: B, 3: D})
+    outs = [o.reshape(n, n) for o in _run("2MM", (n, n, n, n), {0: A, 1: B, 3: D})]
     C_ref = A.astype(np.float64) @ B.astype(np.float64)
     _check(outs[0], C_ref)
     E_ref = outs[0].astype(np.float64) @ D.astype(np.float64)  # second product on the device's C
@@ -94,6 +95,7 @@ def test_syr2k_wide_range():
     B = _wide(rng, (n, m), 3)  # different magnitudes: one shared scale for both pairs
     C = _wide(rng, (n, n), 2)
     (out,) = _run("SYR2K", (n, m), {0: A, 1: B, 2: C})
+    out = out.reshape(n, n)
     a, b = A.astype(np.float64), B.astype(np.float64)
     ref = 12435.0 * (a @ b.T + b @ a.T) + 4546.0 * C.astype(np.float64)
     _check(out, ref)
