@@ -477,7 +477,7 @@ def main() -> int:
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-orders", type=int, default=2, help="orders per kernel in the cpu_baseline sample")
     ap.add_argument("--ref-orders", type=int, default=2, help="orders per kernel per step of --impl reference")
-    ap.add_argument("--sweep-orders", type=int, default=100,
+    ap.add_argument("--sweep-orders", type=int, default=30,
                     help="orders per kernel of the configs[4] sample (explore() on all 15 kernels); 0: skip")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the roofline kernel from an ncu --set full capture")

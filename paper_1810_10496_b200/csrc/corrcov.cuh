@@ -8,10 +8,11 @@
 //          the paper's 5.4x CORR case).
 // stage 1  row-split column statistics (atomics) and the Gram matrix D^T D
 //          as an upper-triangle tiled SIMT GEMM + mirror.
-// stage 2  3xFP16 Gram (m >= 256, n <= kCSMaxRows): three launches -- the
-//          column-strip kernel (statistics, centring, per-column scaled fp16
-//          hi/lo operand rows; strip_stats_f16), the Gram on kind::f16 pair
-//          tiles, the scatter.  Otherwise (3xTF32)
+// stage 2  3xFP16 Gram (m >= 256): the column-strip kernel (statistics,
+//          centring and per-column scaled fp16 hi/lo operand rows in one
+//          launch, strip_stats_f16; for n > kCSMaxRows: colpart + colfinal +
+//          centre_split), the Gram on kind::f16 pair tiles, the scatter.
+//          Otherwise (3xTF32)
 //          four launches: (1) one pass over data accumulates every column's
 //          sum and sum of squares in fp64 (row splits, fp64 atomics) and the
 //          last block of each column finishes mean (and CORR's std) --
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(256) centre_transpose(const float* __restrict_
     }
 }
 
-// ---- stage 2 (3xFP16 Gram): column statistics + centre/scale + operand
+// ---- stage 2 (3xFP16 Gram, n <= kCSMaxRows): column statistics + centre/scale + operand
 // split in ONE launch with no inter-CTA dependency.  A CTA owns a strip of
 // kCS whole columns: all n rows of the strip land in shared memory through
 // cp.async (every 4-byte load in flight at once, no registers), the fp64
@@ -357,12 +358,12 @@ __global__ void __launch_bounds__(kCSThreads, 1)
   __syncthreads();
   // ---- centre (and scale) in place, per-column max|x'|
   {
-    const float mu = mus[c], sc = scs[c];
+    const float mu = mus[c], rsc = 1.f / scs[c];  // (x - mu) * (1 / sc): within an ulp of the division
     float mx = 0.f;
 #pragma unroll 4
     for (int i = g; i < n; i += 16) {
       float x = cs_smem[i * (kCS + 1) + c] - mu;
-      if constexpr (kCorr) x /= sc;
+      if constexpr (kCorr) x *= rsc;
       cs_smem[i * (kCS + 1) + c] = x;
       mx = fmaxf(mx, fabsf(x));
     }
@@ -394,6 +395,144 @@ __global__ void __launch_bounds__(kCSThreads, 1)
       *reinterpret_cast<__half2*>(hrow + i) = hh;  // ldx and i even: 4-byte aligned
       *reinterpret_cast<__half2*>(lrow + i) = ll;
     }
+  }
+}
+
+// ---- stage 2 (3xFP16 Gram, n > kCSMaxRows): three fully parallel launches,
+// data read from HBM once (the strip kernel above was measured faster at
+// 2048^2: 62 vs 71 us for CORR).
+//  (1) colpart: thread per column, 64-row blocks: fp64 S1 (and S2 for CORR)
+//      and the float min / max of the block's rows into partial arrays
+//      [row block][column] (every slot written once: no atomics, no memset).
+//  (2) centre_split: 64 x 64 tiles.  Each CTA finishes the statistics of its
+//      64 columns from the partials in a fixed order (deterministic; mean and
+//      CORR's std exactly as before: sum (x - mu)^2 = S2 - 2 mu S1 + n mu^2
+//      in fp64), bounds max|x'| by max(xmax - mu, mu - xmin) (/ sc for CORR)
+//      to pick each column's power-of-two scale, centres (scales) its tile,
+//      splits it into fp16 hi / lo and writes it transposed: column j of the
+//      data becomes 64 halfs (128 B) of row j of the K-major Gram operand.
+//      The Gram epilogue undoes the column scales exactly.
+constexpr int kPB = 32;  // rows per partial block (all 32 loads of a thread in flight)
+
+template <BenchId Bn, int V, bool kCorr>
+__global__ void __launch_bounds__(256) colpart(const float* __restrict__ data, double* __restrict__ p1,
+                                               double* __restrict__ p2, float* __restrict__ pmin,
+                                               float* __restrict__ pmax, int m, int n) {
+  const int j = blockIdx.x * 256 + threadIdx.x + 1;
+  const int i0 = 1 + blockIdx.y * kPB, i1 = min(n + 1, i0 + kPB);
+  if (j > m) return;
+  double s1 = 0.0, s2 = 0.0;
+  float lo = INFINITY, hi = -INFINITY;
+  float v[kPB];
+#pragma unroll
+  for (int u = 0; u < kPB; ++u) v[u] = i0 + u < i1 ? __ldg(data + (size_t)(i0 + u) * (m + 1) + j) : 0.f;
+#pragma unroll
+  for (int u = 0; u < kPB; ++u)
+    if (i0 + u < i1) {
+      s1 += v[u];
+      if constexpr (kCorr) s2 += (double)v[u] * v[u];
+      lo = fminf(lo, v[u]);
+      hi = fmaxf(hi, v[u]);
+    }
+  const size_t slot = (size_t)blockIdx.y * m + (j - 1);
+  p1[slot] = s1;
+  if constexpr (kCorr) p2[slot] = s2;
+  pmin[slot] = lo;
+  pmax[slot] = hi;
+}
+
+// Statistics of every column once, from the partials: a warp per column
+// (lanes over the row blocks, fixed-order butterfly).  cst[3 j + 0..2] =
+// mu, 1 / sc (CORR), fp16 scale s; mean / std / 1 / s (the Gram epilogue's
+// column factor) written for the compare set and the epilogue.
+template <BenchId Bn, int V, bool kCorr>
+__global__ void __launch_bounds__(256) colfinal(const double* __restrict__ p1, const double* __restrict__ p2,
+                                                const float* __restrict__ pmin, const float* __restrict__ pmax,
+                                                float* mean, float* stdv, float* __restrict__ cst,
+                                                float* __restrict__ rinv, int m, int n) {
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= m) return;
+  const int nb = (n + kPB - 1) / kPB;
+  double s1 = 0.0, s2 = 0.0;
+  float lo = INFINITY, hi = -INFINITY;
+  for (int b = lane; b < nb; b += 32) {
+    const size_t slot = (size_t)b * m + j;
+    s1 += p1[slot];
+    if constexpr (kCorr) s2 += p2[slot];
+    lo = fminf(lo, pmin[slot]);
+    hi = fmaxf(hi, pmax[slot]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    if constexpr (kCorr) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane) return;
+  const float mu = (float)(s1 / (double)kFloatN);
+  float rsc = 1.f;
+  if constexpr (kCorr) {
+    const double qq = s2 - 2.0 * (double)mu * s1 + (double)n * (double)mu * (double)mu;
+    const float sdv = (float)sqrt(fmax(qq, 0.0) / (double)kFloatN);
+    const float sd = sdv <= kEps ? 1.0f : sdv;
+    rsc = 1.f / (sqrtf(kFloatN) * sd);
+    stdv[j + 1] = sd;
+  }
+  mean[j + 1] = mu;
+  const float bound = fmaxf(fmaxf(hi - mu, mu - lo), 0.f) * rsc * 1.0001f;
+  const float sc = f16op::scale_of(bound);
+  cst[3 * j] = mu;
+  cst[3 * j + 1] = rsc;
+  cst[3 * j + 2] = sc;
+  rinv[j] = 1.f / sc;
+}
+
+template <BenchId Bn, int V, bool kCorr>
+__global__ void __launch_bounds__(256) centre_split(const float* __restrict__ data, const float* __restrict__ cst,
+                                                    __half* __restrict__ xh, __half* __restrict__ xl, int m, int n,
+                                                    int ldx) {
+  __shared__ float t[64][65];
+  __shared__ float mu_s[64], rsc_s[64], s16_s[64];
+  const int j0 = blockIdx.x * 64, i0 = blockIdx.y * 64;  // 0-based tile origin (column j0 + c, row i0 + r)
+  // ---- tile: rows i0 .. i0+63 (data rows i0+1 ..), columns j0 .. j0+63 -> transposed halfs;
+  // its loads are issued before the column statistics are fetched
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  float v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int i = i0 + ty + 4 * u, j = j0 + tx;
+    v[u] = (i < n && j < m) ? __ldg(data + (size_t)(i + 1) * (m + 1) + (j + 1)) : 0.f;
+  }
+  if (threadIdx.x < 64) {
+    const int j = min(j0 + (int)threadIdx.x, m - 1);
+    mu_s[threadIdx.x] = cst[3 * j];
+    rsc_s[threadIdx.x] = cst[3 * j + 1];
+    s16_s[threadIdx.x] = cst[3 * j + 2];
+  }
+  __syncthreads();
+  {
+    const float mu = mu_s[tx], rsc = rsc_s[tx];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      float x = v[u] - mu;
+      if constexpr (kCorr) x *= rsc;
+      t[ty + 4 * u][tx] = x;
+    }
+  }
+  __syncthreads();
+  // warp w: operand rows (columns) w, w + 8, ...; lane: halfs 2 lane, +1 of this tile's 64 (128 B)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 2
+  for (int cc = w; cc < 64; cc += 8) {
+    const int j = j0 + cc, i = i0 + 2 * lane;
+    if (j >= m || i >= n) continue;
+    const float s = s16_s[cc];
+    __half2 hh, ll;
+    f16op::split1(t[2 * lane][cc], s, hh.x, ll.x);
+    f16op::split1(i + 1 < n ? t[2 * lane + 1][cc] : 0.f, s, hh.y, ll.y);
+    *reinterpret_cast<__half2*>(xh + (size_t)j * ldx + i) = hh;  // ldx and i even: 4-byte aligned
+    *reinterpret_cast<__half2*>(xl + (size_t)j * ldx + i) = ll;
   }
 }
 
@@ -455,8 +594,10 @@ inline void run(Workspace& ws, cudaStream_t s) {
       const int mp = (m + 3) / 4 * 4, np = (n + 7) / 8 * 8;
       const size_t xs = (size_t)m * np, gs = (size_t)m * mp;
       const int gx = (int)cdiv(m, 256);
+      const int nb = (n + kPB - 1) / kPB;
       float* X = ws.ensure_scratch((2 * xs + gs) * sizeof(float) + 2 * (m + 1) * sizeof(double) + 64 * 4 +
-                                   gx * sizeof(unsigned) + (m + 64) * sizeof(float) + 256);
+                                   gx * sizeof(unsigned) + (m + 64) * sizeof(float) + 512 +
+                                   (size_t)nb * m * (2 * sizeof(double) + 2 * sizeof(float)) + 3 * (size_t)m * sizeof(float));
       if (!X) {
         launch_failed("CORR/COVAR stage 2: scratch allocation failed");
         return;
@@ -469,14 +610,31 @@ inline void run(Workspace& ws, cudaStream_t s) {
       // 3xFP16 Gram (PF_TC_F16=0: 3xTF32) when the column strips fit in
       // shared memory: statistics, centring and the operand split in one
       // launch (strip_stats_f16); else the two-launch fp32 preparation
-      const bool f16 = tc_f16_enabled() && m >= 256 && n <= kCSMaxRows;
+      const bool f16 = tc_f16_enabled() && m >= 256;
       F16Operands f16ops;
-      if (f16) {
+      if (f16 && n <= kCSMaxRows) {
         __half* xh = reinterpret_cast<__half*>(X);
         __half* xl = xh + xs;
         set_smem_attr((const void*)strip_stats_f16<Bn, V, kCorr>, (int)strip_smem(n));
         strip_stats_f16<Bn, V, kCorr><<<cdiv(m, kCS), kCSThreads, strip_smem(n), s>>>(data, mean, stdv, xh, xl,
                                                                                      rinv, m, n, np);
+        f16ops.hi[0] = f16ops.hi[1] = xh;
+        f16ops.lo[0] = f16ops.lo[1] = xl;
+        f16ops.hi[2] = f16ops.hi[3] = f16ops.lo[2] = f16ops.lo[3] = nullptr;
+        f16ops.kp = np;
+        f16ops.rinv = f16ops.cinv = rinv;
+      } else if (f16) {
+        // fp16 images inside X (halfs); column partials after the scale vector
+        __half* xh = reinterpret_cast<__half*>(X);
+        __half* xl = xh + xs;
+        double* p1 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rinv + m + 64) + 255) & ~uintptr_t(255));
+        double* p2 = p1 + (size_t)nb * m;
+        float* pmin = reinterpret_cast<float*>(p2 + (size_t)nb * m);
+        float* pmax = pmin + (size_t)nb * m;
+        float* cst = pmax + (size_t)nb * m;  // [m][3]
+        colpart<Bn, V, kCorr><<<dim3(cdiv(m, 256), nb), 256, 0, s>>>(data, p1, p2, pmin, pmax, m, n);
+        colfinal<Bn, V, kCorr><<<cdiv(m, 8), 256, 0, s>>>(p1, p2, pmin, pmax, mean, stdv, cst, rinv, m, n);
+        centre_split<Bn, V, kCorr><<<dim3(cdiv(m, 64), cdiv(n, 64)), 256, 0, s>>>(data, cst, xh, xl, m, n, np);
         f16ops.hi[0] = f16ops.hi[1] = xh;
         f16ops.lo[0] = f16ops.lo[1] = xl;
         f16ops.hi[2] = f16ops.hi[3] = f16ops.lo[2] = f16ops.lo[3] = nullptr;
@@ -528,9 +686,9 @@ inline void run(Workspace& ws, cudaStream_t s) {
 inline int64_t launches(bool corr, int stage, int64_t m, int64_t n) {
   if (stage == 0) return corr ? 4 : 3;
   const int64_t stats = corr ? 4 : 2;
-  if (stage == 2) {  // [strip statistics + split | stats, centre], Gram, scatter
-    const bool f16 = tc_f16_enabled() && m >= 256 && n <= kCSMaxRows;
-    return (f16 ? 1 : 2) + tc_tma_launches(m, m, n, false, true, true) + 1;
+  if (stage == 2) {  // 3xFP16: partials, statistics, centre + split; else stats, centre; Gram; scatter
+    const bool f16 = tc_f16_enabled() && m >= 256;
+    return (f16 ? (n <= kCSMaxRows ? 1 : 3) : 2) + tc_tma_launches(m, m, n, false, true, true) + 1;
   }
   return stats + 1 + 1 + 1 + (corr ? 1 : 0);
 }

@@ -281,16 +281,16 @@ __device__ __forceinline__ void load_rows(PlaneRows<R, KV>& P, const float* __re
   }
 }
 
-// Linear grid, i-chunk fastest: the CTAs of consecutive chunks of one (k, j)
-// column are launched together, so the two halo planes a chunk shares with
-// its neighbour are read from HBM once and hit L2 the second time (with the
-// chunk index slowest, neighbours ran far apart and inputs larger than L2
-// were read 10/8 times).
+// Linear grid, i-chunk slowest: concurrently resident CTAs stream the same
+// planes (DRAM page locality).  PF_C3_ZFAST=1 (A/B runs) puts the chunk
+// index fastest so a chunk's two halo planes hit L2 when its neighbour reads
+// them -- measured slower at 512^3 (213.0 vs 201.7 us; DRAM reads are 1.03x
+// the algorithmic bytes either way) and equal at 256^3.
 template <BenchId Bn, int V, int R, int PD, int CH, int TX, int TY, int KV>
 __global__ void __launch_bounds__(TX * TY) conv3d_s2d(const float* __restrict__ A, float* __restrict__ B, int ni,
                                                       int nj, int nk, int nchunk, int nbx, int nbxy) {
   constexpr int W = 4 * KV;  // outputs along k per thread
-  // nbxy > 0 (PF_C3_ZSLOW=1, A/B runs): the previous order, chunk slowest
+  // nbxy > 0: chunk slowest (default); nbxy == 0: chunk fastest (PF_C3_ZFAST=1)
   const int chunk = nbxy ? blockIdx.x / nbxy : blockIdx.x % nchunk;
   const int bxy = nbxy ? blockIdx.x % nbxy : blockIdx.x / nchunk;
   const int kq = W * ((bxy % nbx) * TX + threadIdx.x);
@@ -364,8 +364,8 @@ void launch_s2d(const float* A, float* B, int ni, int nj, int nk, cudaStream_t s
     }
   }
   static const bool zslow = [] {
-    const char* e = std::getenv("PF_C3_ZSLOW");
-    return e && e[0] == '1';
+    const char* e = std::getenv("PF_C3_ZFAST");
+    return !(e && e[0] == '1');
   }();
   const int nbx = (int)cdiv(nk, 4 * KV * TX), nby = (int)cdiv(nj - 2, TY * R), nchunk = (int)cdiv(ni - 2, CH);
   conv3d_s2d<B_3DCONV, V, R, PD, CH, TX, TY, KV><<<(unsigned)nbx * nby * nchunk, dim3(TX, TY), 0, s>>>(

@@ -102,8 +102,10 @@ constexpr auto kRun = make_run_table<Run>(std::make_integer_sequence<int, kNV>{}
 int64_t elems(int a, const Dims& d) { return a <= 1 ? d.d[0] * d.d[1] : d.d[0] * d.d[0]; }
 int64_t launches(int v, const Dims& d) {
   if (kTab.v[v].stage != 2) return 1;
-  // symmetric TMA path: two lo split passes + beta pre-pass + GEMM
-  return tma_ok(d.d[1], d.d[1]) ? 4 : tc_launches(d.d[0], d.d[0], d.d[1], false, true);
+  // symmetric TMA path: two lo split passes + beta pre-pass + GEMM (3xFP16:
+  // one paired operand split + beta pre-pass + GEMM)
+  if (tma_ok(d.d[1], d.d[1])) return tc_f16_wanted(d.d[0], d.d[0], d.d[1], true, false, true) ? 3 : 4;
+  return tc_launches(d.d[0], d.d[0], d.d[1], false, true);
 }
 double alg_bytes(const Dims& d) { return 4.0 * (2.0 * d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }
 double alg_flops(const Dims& d) { return 4.0 * (double)d.d[0] * d.d[0] * d.d[1]; }

@@ -15,9 +15,10 @@
 // subnormals; their absolute error stays below 2^-40 of the row max.  The
 // product accumulates lo*hi + hi*lo + hi*hi in the fp32 TMEM accumulator and
 // the epilogue multiplies by alpha / (s_row s_col), exactly (powers of two).
-// Per-row scales need no global reduction: every row is scaled by the warp
-// (K-major) or CTA (MN-major strip) that converts it -- one launch for all
-// operands of a contraction.  K-concatenated products (SYR2K: A B^T + B A^T)
+// Per-row scales need no global reduction: a K-major row is scaled by the
+// warp that converts it, an MN-major column by the CTA that holds its strip
+// (one launch); MN-major operands with K > kStripMaxK take a second launch
+// (column maxima of 32-row blocks, then 64 x 64 tiles transposed).  K-concatenated products (SYR2K: A B^T + B A^T)
 // share one scale per row index across both arrays, so both pairs carry the
 // same s_i s_j.
 #pragma once
@@ -34,7 +35,6 @@ namespace pf {
 namespace f16op {
 
 constexpr int kMaxOps = 4;
-constexpr int kStrip = 16;  // MN-major operands: columns per CTA
 
 struct Op {
   const float* x;   // storage: mn ? K rows x R cols : R rows x K cols, pitch ld (floats)
@@ -46,6 +46,7 @@ struct Op {
   __half* hi2;      // image of x2
   __half* lo2;
   float* rinv;      // [R] 1 / s_row
+  float* part;      // MN-major: per-64-row-block column maxima [ceil(K / 64)][R]
 };
 
 struct Ops {
@@ -97,58 +98,86 @@ __device__ __forceinline__ void store4(__half* hi, __half* lo, float4 v, float s
   *reinterpret_cast<uint2*>(lo) = *reinterpret_cast<const uint2*>(l);
 }
 
-// K-major row r of op (and of x2): warp-cooperative; rows of up to 2048
-// floats stay in registers between the max and the conversion.
+// K-major row r of op (and of x2): warp-cooperative, 2048-float chunks with
+// 16 float4 loads per lane in flight.  Rows of up to 2048 floats stay in
+// registers between the max and the conversion; longer rows are read twice
+// (max pass, then a conversion pass that hits L2).
+template <bool kDual>
+__device__ __forceinline__ void load_chunk(const Op& o, const float* row, const float* row2, int k0, int lane,
+                                           float4 (&v)[16], float4 (&v2)[16]) {
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int k = k0 + 4 * lane + 128 * u;
+    v[u] = k < o.K ? __ldg(reinterpret_cast<const float4*>(row + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (kDual)
+      v2[u] = k < o.K ? __ldg(reinterpret_cast<const float4*>(row2 + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <bool kDual>
+__device__ __forceinline__ void store_chunk(const Op& o, int kp, int r, int k0, int lane, float s,
+                                            const float4 (&v)[16], const float4 (&v2)[16]) {
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int k = k0 + 4 * lane + 128 * u;
+    if (k < o.K) {
+      store4(o.hi + (size_t)r * kp + k, o.lo + (size_t)r * kp + k, v[u], s);
+      if constexpr (kDual) store4(o.hi2 + (size_t)r * kp + k, o.lo2 + (size_t)r * kp + k, v2[u], s);
+    }
+  }
+}
+
 template <bool kDual>
 __device__ __forceinline__ void split_row(const Op& o, int kp, int r, int lane) {
-  constexpr int kRegF4 = 16;  // 16 float4 per lane: K <= 2048
   const float* row = o.x + (size_t)r * o.ld;
   const float* row2 = kDual ? o.x2 + (size_t)r * o.ld : nullptr;
   const bool vec = (o.ld % 4 == 0) && (o.K % 4 == 0) && (reinterpret_cast<uintptr_t>(o.x) % 16 == 0) &&
-                   (!o.x2 || reinterpret_cast<uintptr_t>(o.x2) % 16 == 0);
+                   (!kDual || reinterpret_cast<uintptr_t>(o.x2) % 16 == 0);
   float m = 0.f;
-  if (vec && o.K <= 128 * kRegF4) {
-    float4 v[kRegF4], v2[kRegF4];
+  if (vec) {
+    float4 v[16], v2[16];
+    for (int k0 = 0; k0 < o.K; k0 += 2048) {
+      load_chunk<kDual>(o, row, row2, k0, lane, v, v2);
 #pragma unroll
-    for (int u = 0; u < kRegF4; ++u) {
-      const int k = 4 * lane + 128 * u;
-      v[u] = k < o.K ? __ldg(reinterpret_cast<const float4*>(row + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      v2[u] = (row2 && k < o.K) ? __ldg(reinterpret_cast<const float4*>(row2 + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < 16; ++u) {
+        m = fmaxf(m, amax4(v[u]));
+        if constexpr (kDual) m = fmaxf(m, amax4(v2[u]));
+      }
     }
-#pragma unroll
-    for (int u = 0; u < kRegF4; ++u) m = fmaxf(m, fmaxf(amax4(v[u]), amax4(v2[u])));
     const float s = scale_of(warp_max(m));
     if (lane == 0) o.rinv[r] = 1.f / s;
-#pragma unroll
-    for (int u = 0; u < kRegF4; ++u) {
-      const int k = 4 * lane + 128 * u;
-      if (k < o.K) {
-        store4(o.hi + (size_t)r * kp + k, o.lo + (size_t)r * kp + k, v[u], s);
-        if (row2) store4(o.hi2 + (size_t)r * kp + k, o.lo2 + (size_t)r * kp + k, v2[u], s);
-      }
+    if (o.K <= 2048) {
+      store_chunk<kDual>(o, kp, r, 0, lane, s, v, v2);
+      return;
+    }
+    for (int k0 = 0; k0 < o.K; k0 += 2048) {
+      load_chunk<kDual>(o, row, row2, k0, lane, v, v2);
+      store_chunk<kDual>(o, kp, r, k0, lane, s, v, v2);
     }
     return;
   }
-  // long or unaligned rows: max pass, then a conversion pass (re-read from L1/L2)
+  // unaligned rows: scalar max pass, then a conversion pass
   for (int k = lane; k < o.K; k += 32) {
     m = fmaxf(m, fabsf(__ldg(row + k)));
-    if (row2) m = fmaxf(m, fabsf(__ldg(row2 + k)));
+    if constexpr (kDual) m = fmaxf(m, fabsf(__ldg(row2 + k)));
   }
   const float s = scale_of(warp_max(m));
   if (lane == 0) o.rinv[r] = 1.f / s;
   for (int k = lane; k < o.K; k += 32) {
     split1(__ldg(row + k), s, o.hi[(size_t)r * kp + k], o.lo[(size_t)r * kp + k]);
-    if (row2) split1(__ldg(row2 + k), s, o.hi2[(size_t)r * kp + k], o.lo2[(size_t)r * kp + k]);
+    if constexpr (kDual) split1(__ldg(row2 + k), s, o.hi2[(size_t)r * kp + k], o.lo2[(size_t)r * kp + k]);
   }
 }
 
-// MN-major strip: storage X[k][r], columns r0 .. r0+15 -> image rows r0 ..
-// r0+15 (K halfs each).  K <= kStripMaxK: the whole K x 16 strip lands in
+constexpr int kStrip = 16;  // MN-major strips: columns per CTA
+
+// MN-major strip (K <= kStripMaxK): storage X[k][r], columns r0 .. r0+15 ->
+// image rows r0 .. r0+15 (K halfs each).  The whole K x 16 strip lands in
 // shared memory through cp.async (every 4-byte load in flight at once),
 // per-column max, then each column leaves as one image row (warp w: rows w,
-// w + 8; lane: halfs 2 lane + 64 e, +1 -- 128-byte stores).  Longer K:
-// streamed twice (max pass, then 64-deep blocks transposed through shared
-// memory).
+// w + 8; lane: halfs 2 lane + 64 e, +1 -- 128-byte stores).  One launch;
+// measured faster than the two-pass form below at K = 2048 (2MM 2048:
+// 136 vs 142 us).
 constexpr int kStripMaxK = 2944;  // K * 17 * 4 bytes <= 200 KB
 inline size_t strip_smem_bytes(int K) { return (size_t)K * (kStrip + 1) * sizeof(float); }
 
@@ -158,7 +187,7 @@ __device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* 
   const int t = threadIdx.x, c = t % kStrip, g = t / kStrip;  // 16 x 16
   const int r = r0 + c;
   float m = 0.f;
-  if (o.K <= kStripMaxK) {
+  {
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(strip));
     for (int k = g; k < o.K; k += 16) {
       if (r < o.R)
@@ -172,9 +201,6 @@ __device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* 
     __syncthreads();
 #pragma unroll 4
     for (int k = g; k < o.K; k += 16) m = fmaxf(m, fabsf(strip[k * (kStrip + 1) + c]));
-  } else if (r < o.R) {
-#pragma unroll 8
-    for (int k = g; k < o.K; k += 16) m = fmaxf(m, fabsf(__ldg(o.x + (size_t)k * o.ld + r)));
   }
   red[g][c] = m;
   __syncthreads();
@@ -187,7 +213,7 @@ __device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* 
     if (r0 + t < o.R) o.rinv[r0 + t] = 1.f / s;
   }
   __syncthreads();
-  if (o.K <= kStripMaxK) {
+  {
     const int w = t >> 5, lane = t & 31;
 #pragma unroll 1
     for (int cc = w; cc < kStrip; cc += 8) {
@@ -205,25 +231,29 @@ __device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* 
       }
     }
     __syncthreads();  // the strip buffer is reused by the next strip
-    return;
   }
-  __shared__ __align__(16) __half th[kStrip][64 + 8], tl[kStrip][64 + 8];
-  const float s = sc[c];
-  for (int k0 = 0; k0 < o.K; k0 += 64) {
+}
+
+// MN-major operands with K > kStripMaxK (storage X[k][r], r contiguous) in
+// two fully parallel passes: f16_split computes per-column maxima of 64-row blocks into
+// partials [block][r] (thread per column, 16 loads in flight), then
+// f16_tsplit converts 64 x 64 tiles: each CTA reduces its 64 columns'
+// partials (fixed order), scales, splits and writes the tile transposed
+// (column r -> 128-byte segment of image row r).
+constexpr int kMB = 32;  // rows per partial-max block (all 32 loads of a thread in flight)
+
+__device__ __forceinline__ void colmax_part(const Op& o, float* part, int bx, int nbx) {
+  const int nb = (o.K + kMB - 1) / kMB, nc = (o.R + 255) / 256;
+  for (int job = bx; job < nb * nc; job += nbx) {
+    const int b = job / nc, r = (job % nc) * 256 + threadIdx.x;
+    if (r >= o.R) continue;
+    const int k0 = b * kMB, k1 = min(o.K, k0 + kMB);
+    float m = 0.f, v[kMB];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int kk = g + 16 * u, k = k0 + kk;
-      const float v = (r < o.R && k < o.K) ? __ldg(o.x + (size_t)k * o.ld + r) : 0.f;
-      split1(v, s, th[c][kk], tl[c][kk]);
-    }
-    __syncthreads();
-    // 16 image rows x 64 halfs (128 B) per array: thread -> row t / 16, halfs 4 (t % 16) .. +3
-    const int rr = t / 16, q = t % 16, k = k0 + 4 * q;
-    if (r0 + rr < o.R && k < o.K && k + 4 <= kp) {
-      *reinterpret_cast<uint2*>(o.hi + (size_t)(r0 + rr) * kp + k) = *reinterpret_cast<const uint2*>(&th[rr][4 * q]);
-      *reinterpret_cast<uint2*>(o.lo + (size_t)(r0 + rr) * kp + k) = *reinterpret_cast<const uint2*>(&tl[rr][4 * q]);
-    }
-    __syncthreads();
+    for (int u = 0; u < kMB; ++u) v[u] = k0 + u < k1 ? __ldg(o.x + (size_t)(k0 + u) * o.ld + r) : 0.f;
+#pragma unroll
+    for (int u = 0; u < kMB; ++u) m = fmaxf(m, fabsf(v[u]));
+    part[(size_t)b * o.R + r] = m;
   }
 }
 
@@ -231,14 +261,74 @@ __device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* 
 // CTA); MN-major operands: one 16-column strip per CTA.
 template <BenchId Bn, int V, bool kDual>
 __global__ void __launch_bounds__(256) f16_split(const Ops ops) {
-  extern __shared__ float f16_strip[];  // MN-major strips (dynamic; none when every operand is K-major)
   const Op& o = ops.op[blockIdx.y];
   if (o.mn) {
-    for (int r0 = blockIdx.x * kStrip; r0 < o.R; r0 += gridDim.x * kStrip) split_strip(o, ops.kp, r0, f16_strip);
+    extern __shared__ float f16_strip[];  // K x 17 floats when K <= kStripMaxK
+    if (o.K <= kStripMaxK)
+      for (int r0 = blockIdx.x * kStrip; r0 < o.R; r0 += gridDim.x * kStrip) split_strip(o, ops.kp, r0, f16_strip);
+    else
+      colmax_part(o, o.part, blockIdx.x, gridDim.x);  // pass 1 (f16_tsplit follows)
     return;
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = blockIdx.x * 8 + w; r < o.R; r += gridDim.x * 8) split_row<kDual>(o, ops.kp, r, lane);
+}
+
+// pass 2 of the MN-major operands: blockIdx.y = operand (K-major ones exit)
+template <BenchId Bn, int V>
+__global__ void __launch_bounds__(256) f16_tsplit(const Ops ops) {
+  const Op& o = ops.op[blockIdx.y];
+  if (!o.mn) return;
+  __shared__ float t[64][65];
+  __shared__ float sc[64];
+  __shared__ float red[64][4];
+  const int tr = (o.R + 63) / 64, tk = (o.K + 63) / 64, nb = (o.K + kMB - 1) / kMB;
+  for (int tile = blockIdx.x; tile < tr * tk; tile += gridDim.x) {
+    const int r0 = (tile % tr) * 64, k0 = (tile / tr) * 64;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+    float v[16];  // the tile's loads go out before the partials are reduced
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int k = k0 + ty + 4 * u, r = r0 + tx;
+      v[u] = (k < o.K && r < o.R) ? __ldg(o.x + (size_t)k * o.ld + r) : 0.f;
+    }
+    {  // column scales: 4 threads per column over the row-block partials
+      const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
+      float m = 0.f;
+      if (r0 + c < o.R)
+        for (int b0 = q; b0 < nb; b0 += 4 * 16) {  // 16 partials per thread in flight
+          float pm[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) pm[u] = b0 + 4 * u < nb ? o.part[(size_t)(b0 + 4 * u) * o.R + r0 + c] : 0.f;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) m = fmaxf(m, pm[u]);
+        }
+      red[c][q] = m;
+      __syncthreads();
+      if (threadIdx.x < 64) {
+        const int cc = threadIdx.x;
+        const float s = scale_of(fmaxf(fmaxf(red[cc][0], red[cc][1]), fmaxf(red[cc][2], red[cc][3])));
+        sc[cc] = s;
+        if (k0 == 0 && r0 + cc < o.R) o.rinv[r0 + cc] = 1.f / s;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) t[ty + 4 * u][tx] = v[u];
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 2
+    for (int cc = w; cc < 64; cc += 8) {
+      const int r = r0 + cc, k = k0 + 2 * lane;
+      if (r >= o.R || k >= o.K) continue;
+      const float s = sc[cc];
+      __half2 hh, ll;
+      split1(t[2 * lane][cc], s, hh.x, ll.x);
+      split1(k + 1 < o.K ? t[2 * lane + 1][cc] : 0.f, s, hh.y, ll.y);
+      *reinterpret_cast<__half2*>(o.hi + (size_t)r * ops.kp + k) = hh;  // kp and k even: 4-byte aligned
+      *reinterpret_cast<__half2*>(o.lo + (size_t)r * ops.kp + k) = ll;
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace f16op
@@ -268,7 +358,9 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
   const size_t vec = ((size_t)std::max(a.M, a.N) + 64) * sizeof(float);  // inverse scales (padded)
   const bool same = !dual && a.A == a.B && a.ta == !a.tb && a.M == a.N && a.lda == a.ldb;  // SYRK: A A^T
   const int nimg = dual ? 2 : (same ? 1 : 2);
-  uint8_t* base = reinterpret_cast<uint8_t*>(ws.ensure_scratch(2 * nimg * img + 2 * vec + 256));
+  const size_t partb = (((size_t)(a.K + f16op::kMB - 1) / f16op::kMB) * std::max(a.M, a.N) * sizeof(float) + 255) /
+                       256 * 256;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws.ensure_scratch(2 * nimg * img + 2 * vec + 2 * partb + 256));
   if (!base) return false;
   auto H = [&](int i) { return reinterpret_cast<__half*>(base + i * img); };
   float* rinv_a = reinterpret_cast<float*>(base + 2 * nimg * img);
@@ -297,6 +389,7 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
     f16op::Op& oa = ops.op[0];
     oa.x = a.A, oa.mn = a.ta ? 1 : 0, oa.R = a.M, oa.K = a.K, oa.ld = a.lda;
     oa.hi = H(0), oa.lo = H(1), oa.rinv = rinv_a;
+    oa.part = reinterpret_cast<float*>(base + 2 * nimg * img + 2 * vec);
     ops.n = 1;
     out.hi[0] = H(0), out.lo[0] = H(1);
     out.rinv = rinv_a;
@@ -307,6 +400,7 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
       f16op::Op& ob = ops.op[1];
       ob.x = a.B, ob.mn = a.tb ? 0 : 1, ob.R = a.N, ob.K = a.K, ob.ld = a.ldb;
       ob.hi = H(2), ob.lo = H(3), ob.rinv = rinv_b;
+      ob.part = reinterpret_cast<float*>(base + 2 * nimg * img + 2 * vec + partb);
       ops.n = 2;
       out.hi[1] = H(2), out.lo[1] = H(3);
       out.cinv = rinv_b;
@@ -315,16 +409,24 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
   }
   out.kp = kp;
   const int rows = std::max(a.M, a.N);
-  const int grid = std::max((rows + 7) / 8, (rows + f16op::kStrip - 1) / f16op::kStrip);
-  const dim3 g3(std::min(grid, 8 * device_sms()), ops.n);
   bool any_mn = false;
   for (int i = 0; i < ops.n; ++i) any_mn |= ops.op[i].mn != 0;
-  const size_t smem = any_mn && a.K <= f16op::kStripMaxK ? f16op::strip_smem_bytes(a.K) : 0;
+  // K-major rows: 8 per CTA; MN-major column-max jobs: (K / 64) x (R / 256)
+  const bool strips = a.K <= f16op::kStripMaxK;
+  const int jobs_mn = !any_mn ? 0
+                      : strips ? (rows + f16op::kStrip - 1) / f16op::kStrip
+                               : (int)(((a.K + f16op::kMB - 1) / f16op::kMB) * ((rows + 255) / 256));
+  const int grid = std::min(std::max((rows + 7) / 8, jobs_mn), 8 * device_sms());
+  const size_t smem = any_mn && strips ? f16op::strip_smem_bytes(a.K) : 0;
   if (dual) {
-    f16op::f16_split<Bn, V, true><<<g3, 256, 0, s>>>(ops);
+    f16op::f16_split<Bn, V, true><<<dim3(grid, ops.n), 256, 0, s>>>(ops);
   } else {
     set_smem_attr((const void*)f16op::f16_split<Bn, V, false>, (int)smem);
-    f16op::f16_split<Bn, V, false><<<g3, 256, smem, s>>>(ops);
+    f16op::f16_split<Bn, V, false><<<dim3(grid, ops.n), 256, smem, s>>>(ops);
+  }
+  if (any_mn && !strips) {
+    const int tiles = ((rows + 63) / 64) * ((a.K + 63) / 64);
+    f16op::f16_tsplit<Bn, V><<<dim3(std::min(tiles, 8 * device_sms()), ops.n), 256, 0, s>>>(ops);
   }
   return true;
 }

@@ -73,7 +73,7 @@ struct TmaParams {
   int idesc_override;                 // probe only: -1 auto, else (a_major | b_major << 1)
   int f16;                            // operands are 3xFP16 images (hi/lo fp16, K-major): kind::f16 MMAs
   const float* f16_rinv;              // f16: 1 / row scale per output row (power of two)
-  const float* f16_cinv;              // f16: 1 / row scale of op(B)^T per output column (padded to +64)
+  const float* f16_cinv;              // f16: 1 / row scale of op(B)^T per output column
   int diag;                           // diagnostics only (PF_TC_DIAG): 1 skip lo split, 2 skip MMAs, 4 skip loads, 8 skip epilogue, 16 lane-row epilogue, 32 smem-transpose epilogue
 };
 
@@ -179,6 +179,9 @@ __device__ __forceinline__ void reduce_add_2d(const CUtensorMap* map, uint32_t s
                : "memory");
 }
 
+// ar: alpha, or for 3xFP16 operands alpha / s_row of this lane's row (exact:
+// powers of two); cs_s: the 3xFP16 column factors 1 / s_col of this tile's
+// columns (shared memory, indexed from col0), or nullptr.
 // Epilogue of one warp through TMA (the tile rows row0 .. row0+31 = TMEM
 // lanes, ncols accumulator columns from col0).  The warp's Cin boxes (32x32,
 // SWIZZLE_128B) are requested with one mbarrier before the first TMEM read;
@@ -186,8 +189,9 @@ __device__ __forceinline__ void reduce_add_2d(const CUtensorMap* map, uint32_t s
 // 16 * (j ^ (row % 8)), conflict-free -- and written back by one TMA store
 // (or a TMA add-reduction onto the beta-prescaled D for split-K).  buf:
 // 1024-byte aligned, ncols / 32 * 4 KB; bar: this warp's mbarrier (phase 0).
-__device__ __forceinline__ void epilogue_tma(const TmaParams& p, float alpha, uint32_t taddr, int ncols, int row0,
-                                             int col0, bool split, uint8_t* buf, uint32_t bar, int lane,
+__device__ __forceinline__ void epilogue_tma(const TmaParams& p, float ar, const float* cs_s, uint32_t taddr,
+                                             int ncols, int row0, int col0, bool split, uint8_t* buf, uint32_t bar,
+                                             int lane,
                                              bool writes_done = false, uint8_t* lobuf = nullptr,
                                              bool mirror = false) {
   if (row0 >= p.M) return;  // warp-uniform
@@ -197,8 +201,7 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, float alpha, ui
   const bool want_mirror = mirror && split && lobuf != nullptr;  // same ring: transposed chunks
   const uint32_t sbuf = tc::smem_u32(buf);
   const uint32_t slo = (want_lo || want_mirror) ? tc::smem_u32(lobuf) : 0u;
-  // 3xFP16: undo the power-of-two row scales exactly (alpha / s_row, then / s_col)
-  const float ar = p.f16 ? alpha * __ldg(p.f16_rinv + min(row0 + lane, p.M - 1)) : alpha;
+
   if (use_c && lane == 0) {
     tc::mbar_expect_tx(bar, (uint32_t)nch * 4096u);
     for (int c = 0; c < nch; ++c) load_2d(sbuf + c * 4096, &p.tc, col0 + c * 32, row0, bar);
@@ -214,8 +217,8 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, float alpha, ui
       float4* slot = row + (j ^ (lane & 7));
       float4 v = make_float4(ar * __uint_as_float(r[4 * j]), ar * __uint_as_float(r[4 * j + 1]),
                              ar * __uint_as_float(r[4 * j + 2]), ar * __uint_as_float(r[4 * j + 3]));
-      if (p.f16) {
-        const float4 cs = __ldg(reinterpret_cast<const float4*>(p.f16_cinv + col0 + c * 32 + 4 * j));
+      if (cs_s) {  // 3xFP16: 1 / s_col, staged in shared memory before the accumulator wait
+        const float4 cs = *reinterpret_cast<const float4*>(cs_s + c * 32 + 4 * j);
         v = make_float4(v.x * cs.x, v.y * cs.y, v.z * cs.z, v.w * cs.w);
       }
       if (use_c) {
@@ -262,6 +265,16 @@ __device__ __forceinline__ void epilogue_tma(const TmaParams& p, float alpha, ui
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   __syncwarp();
+}
+
+// 3xFP16: this warp's row factor alpha / s_row and its copy of the tile's
+// column factors (ncols floats from col0), loaded while the mainloop runs.
+__device__ __forceinline__ float stage_f16_scales(const TmaParams& p, int row, int col0, int ncols, float* cs_s,
+                                                  int lane) {
+  if (!p.f16) return p.alpha;
+  for (int c = lane; c < ncols; c += 32) cs_s[c] = col0 + c < p.N ? __ldg(p.f16_cinv + col0 + c) : 1.f;
+  __syncwarp();
+  return p.alpha * __ldg(p.f16_rinv + min(row, p.M - 1));
 }
 
 // Ordered split-K hand-over.  Split 0 of an output tile writes
@@ -324,6 +337,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
   extern __shared__ uint8_t tma_smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar, epi_bar[4];
   __shared__ uint32_t tmem_slot;
+  __shared__ __align__(16) float epi_cs[4][256];  // 3xFP16 column factors, one copy per epilogue warp
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mb = blockIdx.y, nb = blockIdx.x;
@@ -427,14 +441,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tc_tma_kernel(const __grid_con
     }
     // ---- epilogue: TMEM lanes 32*(warp%4) .. +31 are tile rows (coalesced
     // through the idle stage ring, see tc::epilogue_rows32)
+    const int quad = warp & 3;
+    const float ar = tma::stage_f16_scales(p, m0 + quad * 32 + lane, n0, 128, epi_cs[quad], lane);
     tc::mbar_wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
-    const int quad = warp & 3;
     if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
-      tma::epilogue_tma(p, p.alpha, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
+      tma::epilogue_tma(p, ar, p.f16 ? epi_cs[quad] : nullptr, tmem + ((uint32_t)(quad * 32) << 16), 128, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
                         p.sym && nb != mb);
@@ -544,6 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
   extern __shared__ uint8_t tma_smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kTmaStages], ready_bar[kTmaStages], empty_bar[kTmaStages], accum_bar, epi_bar[4];
   __shared__ uint32_t tmem_slot;
+  __shared__ __align__(16) float epi_cs[4][256];  // 3xFP16 column factors, one copy per epilogue warp
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc2::cluster_rank();
@@ -656,14 +672,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTmaThreads, 1)
     }
     // all MMAs of the pair (which read this CTA's ring) have retired once
     // accum fires, so the ring holds the epilogue transpose buffers
+    const int quad = warp & 3;
+    const float ar = tma::stage_f16_scales(p, m0 + quad * 32 + lane, n0, 256, epi_cs[quad], lane);
     tc2::wait(tc::smem_u32(&accum_bar), 0);
     tc::fence_after();
-    const int quad = warp & 3;
     if (p.tma_epi && !(p.diag & (8 | 16 | 32))) {
       const bool ordered = split && p.tile_flags != nullptr;
       if (ordered && blockIdx.z > 0) tma::split_wait(p, lane);
       if (split && !ordered) asm volatile("griddepcontrol.wait;" ::: "memory");  // the beta pre-pass is done
-      tma::epilogue_tma(p, p.alpha, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
+      tma::epilogue_tma(p, ar, p.f16 ? epi_cs[quad] : nullptr, tmem + ((uint32_t)(quad * 32) << 16), 256, m0 + quad * 32, n0,
                         split && !(ordered && blockIdx.z == 0), smem + (size_t)quad * 32768,
                         tc::smem_u32(&epi_bar[quad]), lane, ordered, smem + 131072 + (size_t)quad * 16384,
                         p.sym && nb != mb);
@@ -1021,13 +1038,15 @@ inline bool tc_f16_wanted(const TcGemmArgs& a) {
   return tc_f16_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0, a.sym != 0);
 }
 
-// launches of a 3xFP16 contraction: absmax + split + [beta pre-pass] + gemm
+// launches of a 3xFP16 contraction: split [+ transposing split of an MN-major
+// op(B), as in 2MM / 3MM] + [beta pre-pass] + gemm; symmetric products
+// (K-major operands only): split + beta pre-pass + gemm
 inline int64_t tc_f16_launches(int64_t m, int64_t n, int64_t k, bool dual, bool sym, bool beta_zero = false) {
-  if (sym) return 4;
+  if (sym) return 3;
   const int kblocks = (int)((dual ? 2 : 1) * ((k + 63) / 64));
   const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, false) <= 2;
   const bool split = tc_tma_splits(m, n, kblocks, pair, false) > 1;
-  return 2 + 1 + (split && !beta_zero ? 1 : 0);
+  return (k <= f16op::kStripMaxK ? 1 : 2) + 1 + (split && !beta_zero ? 1 : 0);
 }
 
 // launches of one contraction: [lo passes, one per distinct operand array] +

@@ -49,7 +49,8 @@ def _stage2(bench):
     return next(v for v in range(len(fam.knobs)) if fam.key(v) == "stage=2")
 
 
-def _run(bench, dims, inputs):
+def _run(bench, dims, inputs, arrays):
+    """Stage-2 run on uploaded inputs; returns the requested arrays (by index)."""
     from paper_1810_10496_b200.backend.b200 import Workspace
 
     ws = Workspace(0, bench, dims)
@@ -58,7 +59,7 @@ def _run(bench, dims, inputs):
         for a, x in inputs.items():
             ws.upload(a, x)
         ws.run(_stage2(bench), samples=1, batch=1, restore=False, flush=False)
-        return [ws.download(a) for a, (_, _, o) in enumerate(ws.arrays) if o]
+        return [ws.download(a) for a in arrays]
     finally:
         ws.close()
 
@@ -68,7 +69,7 @@ def test_syrk_wide_range(n, m):
     rng = np.random.default_rng(n + m)
     A = _wide(rng, (n, m))
     C = _wide(rng, (n, n), decades=2)
-    (out,) = _run("SYRK", (n, m), {0: A, 1: C})
+    (out,) = _run("SYRK", (n, m), {0: A, 1: C}, [1])
     out = out.reshape(n, n)
     a64 = A.astype(np.float64)
     ref = 12435.0 * (a64 @ a64.T) + 4546.0 * C.astype(np.float64)
@@ -81,7 +82,7 @@ def test_2mm_wide_range_f16_path():
     A = _wide(rng, (n, n), 6)
     B = _wide(rng, (n, n), 6)
     D = _wide(rng, (n, n), 4)
-    outs = [o.reshape(n, n) for o in _run("2MM", (n, n, n, n), {0: A, 1: B, 3: D})]
+    outs = [o.reshape(n, n) for o in _run("2MM", (n, n, n, n), {0: A, 1: B, 3: D}, [2, 4])]  # C = A B, E = C D
     C_ref = A.astype(np.float64) @ B.astype(np.float64)
     _check(outs[0], C_ref)
     E_ref = outs[0].astype(np.float64) @ D.astype(np.float64)  # second product on the device's C
@@ -94,7 +95,7 @@ def test_syr2k_wide_range():
     A = _wide(rng, (n, m), 6)
     B = _wide(rng, (n, m), 3)  # different magnitudes: one shared scale for both pairs
     C = _wide(rng, (n, n), 2)
-    (out,) = _run("SYR2K", (n, m), {0: A, 1: B, 2: C})
+    (out,) = _run("SYR2K", (n, m), {0: A, 1: B, 2: C}, [2])
     out = out.reshape(n, n)
     a, b = A.astype(np.float64), B.astype(np.float64)
     ref = 12435.0 * (a @ b.T + b @ a.T) + 4546.0 * C.astype(np.float64)
@@ -108,3 +109,39 @@ def test_tf32_mode_and_unfused_statistics_still_match():
                         "tests/test_gpu_parity.py", "-k", "tensor_core"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_2mm_long_k_two_pass_split():
+    """K > kStripMaxK (2944): the MN-major operand takes the two-pass split
+    (column maxima of row blocks, then transposed 64 x 64 tiles)."""
+    ni, nj, nk = 1792, 1792, 3008
+    rng = np.random.default_rng(11)
+    A = _wide(rng, (ni, nk), 4)
+    B = _wide(rng, (nk, nj), 4)
+    D = _wide(rng, (nj, ni), 2)
+    C, E = (o.reshape(ni, -1) for o in _run("2MM", (ni, nj, nk, ni), {0: A, 1: B, 3: D}, [2, 4]))
+    _check(C, A.astype(np.float64) @ B.astype(np.float64))
+    _check(E, C.astype(np.float64) @ D.astype(np.float64))
+
+
+@pytest.mark.parametrize("bench", ["CORR", "COVAR"])
+@pytest.mark.parametrize("dims", [(384, 3008), (512, 700)])
+def test_corrcov_both_statistics_paths(bench, dims):
+    """n <= kCSMaxRows: the column-strip kernel; n > kCSMaxRows: column
+    partials + statistics + tile centring; both against the C oracle on the
+    stock input."""
+    from oracle import oracle as orc
+    from paper_1810_10496_b200.backend.b200 import Workspace
+
+    orc.set_threads(0)
+    ref = orc.reference(bench, dims, True, 1729, -1)
+    ws = Workspace(0, bench, dims)
+    try:
+        ws.generate(True, 1729, -1)
+        ws.run(_stage2(bench), samples=1, batch=1, restore=True, flush=False)
+        outs = [ws.download(a) for a, (_, _, o) in enumerate(ws.arrays) if o]
+    finally:
+        ws.close()
+    assert len(outs) == len(ref)
+    for got, r in zip(outs, ref):
+        _check(got, np.asarray(r))
