@@ -537,38 +537,62 @@ __global__ void __launch_bounds__(256) centre_split(const float* __restrict__ da
 }
 
 // symmat[1 + r][1 + c] = G[min(r,c)][max(r,c)] (pitch ldg) (only G's upper
-// triangle is computed); CORR's diagonal is 1.  Block (32, 8), 64x64 tile.
+// triangle is computed); CORR's diagonal is 1.  Block (32, 8), 64x64 tile:
+// thread (x, y) owns tile rows y + 8q and columns x, x + 32.  Tiles above
+// the diagonal copy straight from registers (no shared memory); tiles below
+// it read the mirrored G tile (coalesced rows) and transpose through shared
+// memory; diagonal tiles mirror within the tile.  Interior tiles take an
+// unpredicated path with per-thread row pointers.
 template <BenchId Bn, int V, bool kCorr>
 __global__ void __launch_bounds__(256) sym_scatter(const float* __restrict__ G, int ldg, float* sym, int m) {
   __shared__ float t[kCT][kCT + 1];
   const int c0 = blockIdx.x * kCT, r0 = blockIdx.y * kCT;
-  const bool lower = r0 > c0;  // tile strictly below the diagonal blocks: read the transposed tile
+  const int x = threadIdx.x, y = threadIdx.y;
+  const bool lower = r0 > c0, diag = r0 == c0;
+  const bool full = r0 + kCT <= m && c0 + kCT <= m;
+  const int gr0 = lower ? c0 : r0, gc0 = lower ? r0 : c0;  // G tile origin (always on/above the diagonal)
+  const size_t ls = (size_t)(m + 1);
+  float v[kCT / 8][2];
+  if (full) {
+    const float* g = G + (size_t)(gr0 + y) * ldg + gc0 + x;
 #pragma unroll
-  for (int q = 0; q < kCT / 8; ++q)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int k = threadIdx.y + 8 * q, x = threadIdx.x + 32 * c;
-      const int gr = (lower ? c0 : r0) + k, gc = (lower ? r0 : c0) + x;
-      if (gr < m && gc < m) t[k][x] = G[(size_t)gr * ldg + gc];
+    for (int q = 0; q < kCT / 8; ++q) {
+      v[q][0] = __ldg(g + (size_t)(8 * q) * ldg);
+      v[q][1] = __ldg(g + (size_t)(8 * q) * ldg + 32);
     }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int gr = gr0 + y + 8 * q, gc = gc0 + x + 32 * c;
+        v[q][c] = (gr < m && gc < m) ? __ldg(G + (size_t)gr * ldg + gc) : 0.f;
+      }
+  }
+  if (!lower && !diag) {  // strictly above the diagonal: symmat tile = G tile
+    float* d = sym + (size_t)(r0 + y + 1) * ls + c0 + x + 1;
+#pragma unroll
+    for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        if (full || (r0 + y + 8 * q < m && c0 + x + 32 * c < m)) d[(size_t)(8 * q) * ls + 32 * c] = v[q][c];
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < kCT / 8; ++q)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) t[y + 8 * q][x + 32 * c] = v[q][c];
   __syncthreads();
+  float* d = sym + (size_t)(r0 + y + 1) * ls + c0 + x + 1;
 #pragma unroll
   for (int q = 0; q < kCT / 8; ++q)
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const int k = threadIdx.y + 8 * q, x = threadIdx.x + 32 * c;
-      const int r = r0 + k, col = c0 + x;
-      if (r < m && col < m) {
-        float v;
-        if (lower)
-          v = t[x][k];
-        else if (r <= col)
-          v = t[k][x];
-        else
-          v = t[x][k];  // diagonal tile, lower half: mirror within the tile
-        if (kCorr && r == col) v = 1.0f;
-        sym[(size_t)(r + 1) * (m + 1) + (col + 1)] = v;
-      }
+      const int k = y + 8 * q, xx = x + 32 * c;  // tile row, tile column
+      if (!full && (r0 + k >= m || c0 + xx >= m)) continue;
+      float val = (lower || k > xx) ? t[xx][k] : t[k][xx];
+      if (kCorr && diag && k == xx) val = 1.0f;
+      d[(size_t)(8 * q) * ls + 32 * c] = val;
     }
 }
 

@@ -18,8 +18,9 @@
 //              vec    128-bit loads where a thread walks contiguous memory
 //   stage 1 -- Blackwell re-mapping: warp-cooperative/coalesced reductions,
 //              smem-tiled SIMT, single-launch streaming
-//   stage 2 -- Blackwell staging: fused single-pass kernels, tcgen05/TMEM 3xTF32
-//              tiles for contractions, CUDA-graph / persistent sequences
+//   stage 2 -- Blackwell staging: fused single-pass kernels, tcgen05/TMEM tiles
+//              for contractions (3xFP16 on kind::f16, or 3xTF32), CUDA-graph /
+//              persistent sequences
 #pragma once
 
 #include <cuda_runtime.h>
