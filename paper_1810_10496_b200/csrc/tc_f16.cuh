@@ -16,8 +16,8 @@
 // product accumulates lo*hi + hi*lo + hi*hi in the fp32 TMEM accumulator and
 // the epilogue multiplies by alpha / (s_row s_col), exactly (powers of two).
 // Per-row scales need no global reduction: a K-major row is scaled by the
-// warp that converts it, an MN-major column by the CTA that holds its strip
-// (one launch); MN-major operands with K > kStripMaxK take a second launch
+// warp that converts it, an MN-major column by the CTA that holds its strip;
+// MN-major operands with K > kStripMaxK (or unaligned) take a second launch
 // (column maxima of 32-row blocks, then 64 x 64 tiles transposed).  K-concatenated products (SYR2K: A B^T + B A^T)
 // share one scale per row index across both arrays, so both pairs carry the
 // same s_i s_j.
@@ -53,6 +53,7 @@ struct Ops {
   Op op[kMaxOps];
   int n;
   int kp;
+  int strips;  // MN-major operands as shared-memory strips (else column maxima + transposed tiles)
 };
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -173,36 +174,44 @@ constexpr int kStrip = 16;  // MN-major strips: columns per CTA
 
 // MN-major strip (K <= kStripMaxK): storage X[k][r], columns r0 .. r0+15 ->
 // image rows r0 .. r0+15 (K halfs each).  The whole K x 16 strip lands in
-// shared memory through cp.async (every 4-byte load in flight at once),
-// per-column max, then each column leaves as one image row (warp w: rows w,
-// w + 8; lane: halfs 2 lane + 64 e, +1 -- 128-byte stores).  One launch;
-// measured faster than the two-pass form below at K = 2048 (2MM 2048:
-// 136 vs 142 us).
-constexpr int kStripMaxK = 2944;  // K * 17 * 4 bytes <= 200 KB
-inline size_t strip_smem_bytes(int K) { return (size_t)K * (kStrip + 1) * sizeof(float); }
+// shared memory through 16-byte cp.async (pitch 20 floats; a warp request
+// covers 8 rows x 64 B, so the load is not limited by outstanding 4-byte
+// requests as the first, pitch-17 form was: 15 us for a 2048^2 operand),
+// per-column max, then 256-row chunks are converted row-wise (float4 reads)
+// into a transposed half buffer and leave as 16-byte stores of image rows.
+constexpr int kStripMaxK = 2048;  // K * 20 * 4 + 2 * 16 * 256 * 2 bytes <= 180 KB
+constexpr int kSP = 20;           // strip pitch (floats): 16-byte aligned rows
+constexpr int kSC = 256;          // rows per conversion chunk
+inline size_t strip_smem_bytes(int K) {
+  return (size_t)K * kSP * sizeof(float) + 2 * (size_t)kStrip * (kSC + 8) * sizeof(__half);
+}
 
 __device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* strip) {
   __shared__ float red[16][kStrip + 1];
   __shared__ float sc[kStrip];
-  const int t = threadIdx.x, c = t % kStrip, g = t / kStrip;  // 16 x 16
-  const int r = r0 + c;
-  float m = 0.f;
-  {
+  __half* th = reinterpret_cast<__half*>(strip + (size_t)o.K * kSP);  // [16][kSC + 8]
+  __half* tl = th + kStrip * (kSC + 8);
+  const int t = threadIdx.x;
+  {  // load: thread (chunk q, row group g): 16 bytes at rows g, g + 64, ...
+    const int q = t & 3, g = t >> 2;
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(strip));
-    for (int k = g; k < o.K; k += 16) {
-      if (r < o.R)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sbase + 4u * (uint32_t)(k * (kStrip + 1) + c)),
-                     "l"(o.x + (size_t)k * o.ld + r)
-                     : "memory");
-      else
-        strip[k * (kStrip + 1) + c] = 0.f;
+    const int valid = min(4, max(0, o.R - (r0 + 4 * q)));  // columns of this chunk inside the operand
+    for (int k = g; k < o.K; k += 64) {
+      const float* src = o.x + (size_t)k * o.ld + r0 + 4 * q;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sbase + 4u * (uint32_t)(k * kSP + 4 * q)),
+                   "l"(valid ? src : o.x), "r"(4 * valid)
+                   : "memory");
     }
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-    __syncthreads();
-#pragma unroll 4
-    for (int k = g; k < o.K; k += 16) m = fmaxf(m, fabsf(strip[k * (kStrip + 1) + c]));
   }
-  red[g][c] = m;
+  __syncthreads();
+  {
+    const int c = t % kStrip, g = t / kStrip;  // 16 x 16
+    float m = 0.f;
+#pragma unroll 4
+    for (int k = g; k < o.K; k += 16) m = fmaxf(m, fabsf(strip[k * kSP + c]));
+    red[g][c] = m;
+  }
   __syncthreads();
   if (t < kStrip) {
     float mm = 0.f;
@@ -213,24 +222,36 @@ __device__ __forceinline__ void split_strip(const Op& o, int kp, int r0, float* 
     if (r0 + t < o.R) o.rinv[r0 + t] = 1.f / s;
   }
   __syncthreads();
-  {
-    const int w = t >> 5, lane = t & 31;
-#pragma unroll 1
-    for (int cc = w; cc < kStrip; cc += 8) {
-      if (r0 + cc >= o.R) break;
-      const float s = sc[cc];
-      __half* hrow = o.hi + (size_t)(r0 + cc) * kp;
-      __half* lrow = o.lo + (size_t)(r0 + cc) * kp;
-#pragma unroll 4
-      for (int k = 2 * lane; k < o.K; k += 64) {
-        __half2 hh, ll;
-        split1(strip[k * (kStrip + 1) + cc], s, hh.x, ll.x);
-        split1(k + 1 < o.K ? strip[(k + 1) * (kStrip + 1) + cc] : 0.f, s, hh.y, ll.y);
-        *reinterpret_cast<__half2*>(hrow + k) = hh;  // kp and k even: 4-byte aligned
-        *reinterpret_cast<__half2*>(lrow + k) = ll;
+  const int q = t & 3;
+  const float s0 = sc[4 * q], s1 = sc[4 * q + 1], s2 = sc[4 * q + 2], s3 = sc[4 * q + 3];
+  for (int k0 = 0; k0 < o.K; k0 += kSC) {
+    // row-wise conversion: thread (chunk q, row t / 4 + 64 u) -> transposed halfs
+#pragma unroll
+    for (int u = 0; u < kSC / 64; ++u) {
+      const int kk = (t >> 2) + 64 * u, k = k0 + kk;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < o.K) v = *reinterpret_cast<const float4*>(strip + k * kSP + 4 * q);
+      split1(v.x, s0, th[(4 * q + 0) * (kSC + 8) + kk], tl[(4 * q + 0) * (kSC + 8) + kk]);
+      split1(v.y, s1, th[(4 * q + 1) * (kSC + 8) + kk], tl[(4 * q + 1) * (kSC + 8) + kk]);
+      split1(v.z, s2, th[(4 * q + 2) * (kSC + 8) + kk], tl[(4 * q + 2) * (kSC + 8) + kk]);
+      split1(v.w, s3, th[(4 * q + 3) * (kSC + 8) + kk], tl[(4 * q + 3) * (kSC + 8) + kk]);
+    }
+    __syncthreads();
+    // 16 image rows x kSC halfs per array: thread -> row t / 16, 16-byte pieces (t % 16) + 16 e
+    const int rr = t / 16, piece = t % 16;
+    if (r0 + rr < o.R) {
+#pragma unroll
+      for (int e = 0; e < kSC / 8 / 16; ++e) {
+        const int kk = 8 * (piece + 16 * e), k = k0 + kk;
+        if (k < o.K) {  // kp is a multiple of 8: whole 16-byte pieces stay inside the row
+          *reinterpret_cast<uint4*>(o.hi + (size_t)(r0 + rr) * kp + k) =
+              *reinterpret_cast<const uint4*>(th + rr * (kSC + 8) + kk);
+          *reinterpret_cast<uint4*>(o.lo + (size_t)(r0 + rr) * kp + k) =
+              *reinterpret_cast<const uint4*>(tl + rr * (kSC + 8) + kk);
+        }
       }
     }
-    __syncthreads();  // the strip buffer is reused by the next strip
+    __syncthreads();
   }
 }
 
@@ -263,8 +284,8 @@ template <BenchId Bn, int V, bool kDual>
 __global__ void __launch_bounds__(256) f16_split(const Ops ops) {
   const Op& o = ops.op[blockIdx.y];
   if (o.mn) {
-    extern __shared__ float f16_strip[];  // K x 17 floats when K <= kStripMaxK
-    if (o.K <= kStripMaxK)
+    extern __shared__ float f16_strip[];  // strip_smem_bytes(K) when ops.strips
+    if (ops.strips)
       for (int r0 = blockIdx.x * kStrip; r0 < o.R; r0 += gridDim.x * kStrip) split_strip(o, ops.kp, r0, f16_strip);
     else
       colmax_part(o, o.part, blockIdx.x, gridDim.x);  // pass 1 (f16_tsplit follows)
@@ -409,25 +430,39 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
   }
   out.kp = kp;
   const int rows = std::max(a.M, a.N);
-  bool any_mn = false;
-  for (int i = 0; i < ops.n; ++i) any_mn |= ops.op[i].mn != 0;
-  // K-major rows: 8 per CTA; MN-major column-max jobs: (K / 64) x (R / 256)
-  const bool strips = a.K <= f16op::kStripMaxK;
-  const int jobs_mn = !any_mn ? 0
-                      : strips ? (rows + f16op::kStrip - 1) / f16op::kStrip
-                               : (int)(((a.K + f16op::kMB - 1) / f16op::kMB) * ((rows + 255) / 256));
-  const int grid = std::min(std::max((rows + 7) / 8, jobs_mn), 8 * device_sms());
-  const size_t smem = any_mn && strips ? f16op::strip_smem_bytes(a.K) : 0;
+  bool any_mn = false, any_k = false;
+  for (int i = 0; i < ops.n; ++i) (ops.op[i].mn ? any_mn : any_k) = true;
+  bool aligned = true;  // 16-byte cp.async of the MN-major operands
+  for (int i = 0; i < ops.n; ++i)
+    if (ops.op[i].mn) aligned &= reinterpret_cast<uintptr_t>(ops.op[i].x) % 16 == 0 && ops.op[i].ld % 4 == 0;
+  const bool strips = any_mn && aligned && a.K <= f16op::kStripMaxK;
+  ops.strips = strips ? 1 : 0;
+  const int kgrid = std::min((rows + 7) / 8, 8 * device_sms());  // K-major rows: 8 per CTA
   if (dual) {
-    f16op::f16_split<Bn, V, true><<<dim3(grid, ops.n), 256, 0, s>>>(ops);
-  } else {
-    set_smem_attr((const void*)f16op::f16_split<Bn, V, false>, (int)smem);
-    f16op::f16_split<Bn, V, false><<<dim3(grid, ops.n), 256, smem, s>>>(ops);
+    f16op::f16_split<Bn, V, true><<<dim3(kgrid, ops.n), 256, 0, s>>>(ops);
+    return true;
   }
-  if (any_mn && !strips) {
+  if (strips) {
+    // two launches: the strips' shared memory would hold the K-major CTAs to
+    // one per SM (2MM 2048: 21 us for one shared launch)
+    f16op::Ops km = ops, mn = ops;
+    km.n = mn.n = 0;
+    for (int i = 0; i < ops.n; ++i) (ops.op[i].mn ? mn.op[mn.n++] : km.op[km.n++]) = ops.op[i];
+    if (km.n) f16op::f16_split<Bn, V, false><<<dim3(kgrid, km.n), 256, 0, s>>>(km);
+    const size_t smem = f16op::strip_smem_bytes(a.K);
+    set_smem_attr((const void*)f16op::f16_split<Bn, V, false>, (int)smem);
+    f16op::f16_split<Bn, V, false><<<dim3(std::min((rows + f16op::kStrip - 1) / f16op::kStrip, 8 * device_sms()), mn.n),
+                                     256, smem, s>>>(mn);
+    return true;
+  }
+  // K-major rows and (for long K) the column-max pass in one launch, then the transposed tiles
+  const int jobs_mn = any_mn ? (int)(((a.K + f16op::kMB - 1) / f16op::kMB) * ((rows + 255) / 256)) : 0;
+  f16op::f16_split<Bn, V, false><<<dim3(std::min(std::max(kgrid, jobs_mn), 8 * device_sms()), ops.n), 256, 0, s>>>(ops);
+  if (any_mn) {
     const int tiles = ((rows + 63) / 64) * ((a.K + 63) / 64);
     f16op::f16_tsplit<Bn, V><<<dim3(std::min(tiles, 8 * device_sms()), ops.n), 256, 0, s>>>(ops);
   }
+  (void)any_k;
   return true;
 }
 

@@ -1046,7 +1046,7 @@ inline int64_t tc_f16_launches(int64_t m, int64_t n, int64_t k, bool dual, bool 
   const int kblocks = (int)((dual ? 2 : 1) * ((k + 63) / 64));
   const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, false) <= 2;
   const bool split = tc_tma_splits(m, n, kblocks, pair, false) > 1;
-  return (k <= f16op::kStripMaxK ? 1 : 2) + 1 + (split && !beta_zero ? 1 : 0);
+  return 2 + 1 + (split && !beta_zero ? 1 : 0);  // [K-major rows, MN strips | rows + column maxima, tiles]
 }
 
 // launches of one contraction: [lo passes, one per distinct operand array] +
