@@ -298,7 +298,8 @@ inline size_t strip_smem(int n) { return (size_t)n * (kCS + 1) * sizeof(float); 
 template <BenchId Bn, int V, bool kCorr>
 __global__ void __launch_bounds__(kCSThreads, 1)
     strip_stats_f16(const float* __restrict__ data, float* mean, float* stdv, __half* __restrict__ xh,
-                    __half* __restrict__ xl, float* __restrict__ rinv, int m, int n, int ldx) {
+                    __half* __restrict__ xl, float* __restrict__ rinv, int m, int n, int ldx, float* __restrict__ G,
+                    int ldg) {
   extern __shared__ float cs_smem[];  // [n][kCS + 1]
   __shared__ double r1[16][kCS], r2[16][kCS];
   __shared__ float rmax[16][kCS], mus[kCS], scs[kCS], s16[kCS];
@@ -379,6 +380,17 @@ __global__ void __launch_bounds__(kCSThreads, 1)
     if (j0 + t < m) rinv[j0 + t] = 1.f / s;
   }
   __syncthreads();
+  // ---- zero this strip's rows of the Gram's upper pair tiles (columns from the
+  // row's 256-block on): both split-K halves then add-reduce, no ordered wait
+  {
+    const int w = t >> 5, lane = t & 31;
+    for (int cc = w; cc < kCS; cc += kCSThreads / 32) {
+      const int row = j0 + cc;
+      if (row >= m) break;
+      float4* g4 = reinterpret_cast<float4*>(G + (size_t)row * ldg);
+      for (int c4 = (row / 256) * 64 + lane; c4 < ldg / 4; c4 += 32) g4[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
   // ---- each column -> one operand row (warp w: columns w, w + 8; lane: rows 2 lane + 64 e, +1)
   const int w = t >> 5, lane = t & 31;
 #pragma unroll 1
@@ -641,7 +653,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
         __half* xl = xh + xs;
         set_smem_attr((const void*)strip_stats_f16<Bn, V, kCorr>, (int)strip_smem(n));
         strip_stats_f16<Bn, V, kCorr><<<cdiv(m, kCS), kCSThreads, strip_smem(n), s>>>(data, mean, stdv, xh, xl,
-                                                                                     rinv, m, n, np);
+                                                                                     rinv, m, n, np, G, mp);
         f16ops.hi[0] = f16ops.hi[1] = xh;
         f16ops.lo[0] = f16ops.lo[1] = xl;
         f16ops.hi[2] = f16ops.hi[3] = f16ops.lo[2] = f16ops.lo[3] = nullptr;
@@ -677,6 +689,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
       TcGemmArgs g{m, m, n, 1.f, 0.f, X, np, false, X, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
       if (f16) {
         g.f16 = &f16ops;
+        g.d_zeroed = n <= kCSMaxRows;  // the strip kernel zeroed G's upper tiles
       } else {
         g.Alo = Xlo;
         g.Blo = Xlo;

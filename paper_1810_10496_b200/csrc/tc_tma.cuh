@@ -910,9 +910,10 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   // ordered hand-over only where the alternative pre-pass is a memset (beta
   // == 0): with beta != 0 split 0's Cin load + store serialise the splits
   // (GEMM 512^3: 17.4 us vs 15.3 us with the beta pre-pass)
-  const bool ordered = zs > 1 && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlagsGemm &&
+  const bool zeroed = a.d_zeroed && a.beta == 0.f && !p.sym && p.tma_epi;
+  const bool ordered = zs > 1 && !zeroed && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlagsGemm &&
                        a.beta == 0.f;
-  const bool prepass = (zs > 1 || p.sym) && !ordered;  // beta * Cin (or zero) before the adds
+  const bool prepass = (zs > 1 || p.sym) && !ordered && !zeroed;  // beta * Cin (or zero) before the adds
   p.tile_flags = ordered ? a.tile_flags : nullptr;
   p.epoch = a.epoch;
   if (prepass) {
