@@ -689,7 +689,7 @@ inline void run(Workspace& ws, cudaStream_t s) {
       TcGemmArgs g{m, m, n, 1.f, 0.f, X, np, false, X, np, true, nullptr, nullptr, nullptr, mp, G, mp, 1};
       if (f16) {
         g.f16 = &f16ops;
-        g.d_zeroed = n <= kCSMaxRows;  // the strip kernel zeroed G's upper tiles
+        g.d_base = n <= kCSMaxRows;  // the strip kernel zeroed G's upper tiles (beta = 0)
       } else {
         g.Alo = Xlo;
         g.Blo = Xlo;

@@ -103,8 +103,8 @@ int64_t elems(int a, const Dims& d) { return a <= 1 ? d.d[0] * d.d[1] : d.d[0] *
 int64_t launches(int v, const Dims& d) {
   if (kTab.v[v].stage != 2) return 1;
   // symmetric TMA path: two lo split passes + beta pre-pass + GEMM (3xFP16:
-  // one paired operand split + beta pre-pass + GEMM)
-  if (tma_ok(d.d[1], d.d[1])) return tc_f16_wanted(d.d[0], d.d[0], d.d[1], true, false, true) ? 3 : 4;
+  // one paired operand split carrying the beta pre-pass + GEMM)
+  if (tma_ok(d.d[1], d.d[1])) return tc_f16_wanted(d.d[0], d.d[0], d.d[1], true, false, true) ? 2 : 4;
   return tc_launches(d.d[0], d.d[0], d.d[1], false, true);
 }
 double alg_bytes(const Dims& d) { return 4.0 * (2.0 * d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }

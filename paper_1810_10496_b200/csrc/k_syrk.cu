@@ -63,8 +63,8 @@ int64_t elems(int a, const Dims& d) { return a == 0 ? d.d[0] * d.d[1] : d.d[0] *
 int64_t launches(int v, const Dims& d) {
   if (kTab.v[v].stage != 2) return 1;
   // symmetric TMA path: lo split pass + beta pre-pass + GEMM
-  // (3xFP16: operand split + beta pre-pass + GEMM, also 3)
-  if (tma_ok(d.d[1], d.d[1])) return 3;
+  // (3xFP16: operand split with the beta pre-pass in the same launch + GEMM)
+  if (tma_ok(d.d[1], d.d[1])) return tc_f16_wanted(d.d[0], d.d[0], d.d[1], false, false, true) ? 2 : 3;
   return tc_launches(d.d[0], d.d[0], d.d[1], false, false, 1);
 }
 double alg_bytes(const Dims& d) { return 4.0 * ((double)d.d[0] * d.d[1] + 2.0 * d.d[0] * d.d[0]); }

@@ -54,6 +54,11 @@ struct Ops {
   int n;
   int kp;
   int strips;  // MN-major operands as shared-memory strips (else column maxima + transposed tiles)
+  // optional beta pre-pass riding along in the blockIdx.y == n slice: D = beta * Cin
+  float4* pre_d;
+  const float4* pre_c;
+  int64_t pre_n4;
+  float pre_beta;
 };
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -282,6 +287,24 @@ __device__ __forceinline__ void colmax_part(const Op& o, float* part, int bx, in
 // CTA); MN-major operands: one 16-column strip per CTA.
 template <BenchId Bn, int V, bool kDual>
 __global__ void __launch_bounds__(256) f16_split(const Ops ops) {
+  if ((int)blockIdx.y == ops.n) {  // the contraction's beta pre-pass (symmetric products), 4 loads in flight
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < ops.pre_n4; i += 4 * stride) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(ops.pre_c + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        ops.pre_d[i + u * stride] = make_float4(ops.pre_beta * v[u].x, ops.pre_beta * v[u].y,
+                                                ops.pre_beta * v[u].z, ops.pre_beta * v[u].w);
+    }
+    for (; i < ops.pre_n4; i += stride) {
+      const float4 v = __ldg(ops.pre_c + i);
+      ops.pre_d[i] = make_float4(ops.pre_beta * v.x, ops.pre_beta * v.y, ops.pre_beta * v.z, ops.pre_beta * v.w);
+    }
+    return;
+  }
   const Op& o = ops.op[blockIdx.y];
   if (o.mn) {
     extern __shared__ float f16_strip[];  // strip_smem_bytes(K) when ops.strips
@@ -369,8 +392,11 @@ inline bool tc_f16_enabled() {
 // `out`.  Distinct operand arrays get one image each (SYRK's A serves both
 // sides); a K-concatenated product (A2, B2 = B, A: SYR2K) converts A and B
 // as one paired operand with shared row scales.
+// base_d: also write D = beta * Cin (flat, same shape) inside the K-major
+// launch -- the beta pre-pass of a symmetric product, off the critical path
+// of its own launch; the caller then marks D as based (TcGemmArgs::d_base).
 template <BenchId Bn, int V>
-inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cudaStream_t s) {
+inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cudaStream_t s, bool base_d = false) {
   const bool dual = a.A2 != nullptr;
   if (dual && !(a.A2 == a.B && a.B2 == a.A && !a.ta && a.tb && a.M == a.N && a.lda == a.ldb))
     return false;  // only the symmetric K-concatenation (A B^T + B A^T) shares row scales
@@ -438,8 +464,15 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
   const bool strips = any_mn && aligned && a.K <= f16op::kStripMaxK;
   ops.strips = strips ? 1 : 0;
   const int kgrid = std::min((rows + 7) / 8, 8 * device_sms());  // K-major rows: 8 per CTA
+  const int pre = base_d ? 1 : 0;
+  if (base_d) {
+    ops.pre_d = reinterpret_cast<float4*>(a.D);
+    ops.pre_c = reinterpret_cast<const float4*>(a.Cin);
+    ops.pre_n4 = (int64_t)a.M * a.N / 4;
+    ops.pre_beta = a.beta;
+  }
   if (dual) {
-    f16op::f16_split<Bn, V, true><<<dim3(kgrid, ops.n), 256, 0, s>>>(ops);
+    f16op::f16_split<Bn, V, true><<<dim3(kgrid, ops.n + pre), 256, 0, s>>>(ops);
     return true;
   }
   if (strips) {
@@ -448,7 +481,8 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
     f16op::Ops km = ops, mn = ops;
     km.n = mn.n = 0;
     for (int i = 0; i < ops.n; ++i) (ops.op[i].mn ? mn.op[mn.n++] : km.op[km.n++]) = ops.op[i];
-    if (km.n) f16op::f16_split<Bn, V, false><<<dim3(kgrid, km.n), 256, 0, s>>>(km);
+    mn.pre_n4 = 0;
+    if (km.n || pre) f16op::f16_split<Bn, V, false><<<dim3(kgrid, km.n + pre), 256, 0, s>>>(km);
     const size_t smem = f16op::strip_smem_bytes(a.K);
     set_smem_attr((const void*)f16op::f16_split<Bn, V, false>, (int)smem);
     f16op::f16_split<Bn, V, false><<<dim3(std::min((rows + f16op::kStrip - 1) / f16op::kStrip, 8 * device_sms()), mn.n),
@@ -457,7 +491,8 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
   }
   // K-major rows and (for long K) the column-max pass in one launch, then the transposed tiles
   const int jobs_mn = any_mn ? (int)(((a.K + f16op::kMB - 1) / f16op::kMB) * ((rows + 255) / 256)) : 0;
-  f16op::f16_split<Bn, V, false><<<dim3(std::min(std::max(kgrid, jobs_mn), 8 * device_sms()), ops.n), 256, 0, s>>>(ops);
+  f16op::f16_split<Bn, V, false><<<dim3(std::min(std::max(kgrid, jobs_mn), 8 * device_sms()), ops.n + pre), 256, 0,
+                                   s>>>(ops);
   if (any_mn) {
     const int tiles = ((rows + 63) / 64) * ((a.K + 63) / 64);
     f16op::f16_tsplit<Bn, V><<<dim3(std::min(tiles, 8 * device_sms()), ops.n), 256, 0, s>>>(ops);

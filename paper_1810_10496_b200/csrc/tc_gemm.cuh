@@ -75,9 +75,10 @@ struct TcGemmArgs {
   int sym = 0;
   // 3xFP16 operand images (nullptr: fp32 operands, 3xTF32)
   const F16Operands* f16 = nullptr;
-  // D already holds zeros on every tile the product writes (beta = 0): split-K
-  // partials all add-reduce, with no pre-pass and no ordered hand-over
-  int d_zeroed = 0;
+  // D already holds its base on every tile the product writes -- beta * Cin,
+  // or zeros when beta = 0: split-K partials and symmetric mirrors all
+  // add-reduce, with no pre-pass and no ordered hand-over
+  int d_base = 0;
 };
 
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;

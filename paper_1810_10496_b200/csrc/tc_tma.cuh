@@ -910,7 +910,7 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   // ordered hand-over only where the alternative pre-pass is a memset (beta
   // == 0): with beta != 0 split 0's Cin load + store serialise the splits
   // (GEMM 512^3: 17.4 us vs 15.3 us with the beta pre-pass)
-  const bool zeroed = a.d_zeroed && a.beta == 0.f && !p.sym && p.tma_epi;
+  const bool zeroed = a.d_base && p.tma_epi && (p.sym || zs > 1);  // every write is an add-reduction
   const bool ordered = zs > 1 && !zeroed && !p.sym && p.tma_epi && a.tile_flags && grid_tiles <= kTileFlagsGemm &&
                        a.beta == 0.f;
   const bool prepass = (zs > 1 || p.sym) && !ordered && !zeroed;  // beta * Cin (or zero) before the adds
@@ -1043,7 +1043,7 @@ inline bool tc_f16_wanted(const TcGemmArgs& a) {
 // op(B), as in 2MM / 3MM] + [beta pre-pass] + gemm; symmetric products
 // (K-major operands only): split + beta pre-pass + gemm
 inline int64_t tc_f16_launches(int64_t m, int64_t n, int64_t k, bool dual, bool sym, bool beta_zero = false) {
-  if (sym) return 3;
+  if (sym) return 2;  // split (+ the beta pre-pass in the same launch) + gemm
   const int kblocks = (int)((dual ? 2 : 1) * ((k + 63) / 64));
   const bool pair = tc_pair_ok(m, n) && tc_tma_splits(m, n, kblocks, true, false) <= 2;
   const bool split = tc_tma_splits(m, n, kblocks, pair, false) > 1;
@@ -1070,9 +1070,14 @@ inline bool launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t
   // 3xFP16 operand images for the products that would run pre-split
   if (tc_f16_wanted(a)) {
     F16Operands f;
-    if (prepare_f16<Bn, V>(ws, a, f, s)) {
+    // symmetric products (beta pre-pass + add-reductions): the pre-pass rides
+    // in the operand-split launch when D and Cin are flat, aligned and identical in shape
+    const bool base_d = a.sym && a.Cin && a.ldd == a.N && a.ldc == a.N && a.N % 4 == 0 &&
+                        reinterpret_cast<uintptr_t>(a.D) % 16 == 0 && reinterpret_cast<uintptr_t>(a.Cin) % 16 == 0;
+    if (prepare_f16<Bn, V>(ws, a, f, s, base_d)) {
       TcGemmArgs b = a;
       b.f16 = &f;
+      b.d_base = base_d ? 1 : 0;
       b.Alo = b.Blo = b.A2lo = b.B2lo = nullptr;
       b.Dlo = nullptr;
       if (launch_tc_tma<Bn, V>(b, s)) return false;
