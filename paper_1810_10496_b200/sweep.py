@@ -31,7 +31,7 @@ from . import _abi, passmodel, registry
 from .backend.b200 import B200Backend, Workspace, family, variant_launches
 from .catalog import PassCatalog, PhaseOrder, random_phase_order
 from .dist import shard
-from .explorer import ExplorationConfig, draw_orders, explore
+from .explorer import ExplorationConfig, draw_orders, explore, remember_orders, stream_key
 
 
 @dataclass(frozen=True)
@@ -104,10 +104,15 @@ def evaluate_round(items: list[tuple[Workspace, int]], restore: bool = True, flu
 
 def _lazy_orders(catalog: PassCatalog, config: ExplorationConfig):
     """``draw_orders(catalog, config)`` one order at a time (same RNG use,
-    explorer.py:163-167), so batches can start before the stream is drawn."""
+    explorer.py:163-167), so batches can start before the stream is drawn;
+    the finished stream is remembered for ``explore``'s own draw."""
     rng = Random(config.seed)
+    drawn = []
     for _ in range(config.num_sequences):
-        yield random_phase_order(catalog, config.max_len, rng)
+        order = random_phase_order(catalog, config.max_len, rng)
+        drawn.append(order)
+        yield order
+    remember_orders(stream_key(catalog, config), drawn)
 
 
 def explore_suite(kernels, catalog: PassCatalog, configs, backend: B200Backend, host_inputs: dict | None = None):
