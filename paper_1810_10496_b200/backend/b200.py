@@ -554,6 +554,31 @@ class B200Backend(Backend):
         self._count(ws.bench, variant, ws.dims, samples * batch)
         return ms
 
+    def prewarm(self, kernel: KernelCase) -> int:
+        """Give every variant of ``kernel``'s family its first-use warm-up
+        (module load, scratch, graph capture, batch sizing: the two untimed
+        runs ``_timed`` / the prefetch do on first use) at the measurement
+        size, so later measurements are steady-state.  Returns the number of
+        variants warmed."""
+        bench = registry.bench_of(kernel)
+        _, mdims = registry.parse_descriptor(kernel.measurement_input)
+        ws = self.workspace(bench, mdims, True, -1)
+        n = 0
+        for v in range(len(family(bench).knobs)):
+            if v in ws.warm or not self._supported(bench, v, mdims):
+                continue
+            ws.run(v, samples=1, batch=1, restore=True, flush=False)
+            first = ws.run(v, samples=1, batch=1, restore=True, flush=False)[0]
+            self._count(bench, v, mdims, 2)
+            ws.warm.add(v)
+            key = (bench, ws.dims, v)
+            self._first_ms[key] = first
+            if key not in self._batch:
+                self._batch[key] = (min(self.max_batch, max(1, int(self.min_sample_ms / max(first, 1e-4)) + 1))
+                                    if first < self.min_sample_ms else 1)
+            n += 1
+        return n
+
     # ------------------------------------------------------------ batched evaluation
     def prefetch(self, kernel: KernelCase, orders) -> int:
         """``explore(..., prefetch=True)`` hook: batch the fresh evaluations of

@@ -246,6 +246,26 @@ int occupancy(const void* fn, int threads, size_t smem) {
   return per_sm;
 }
 
+cudaStream_t Workspace::fork(cudaStream_t s) {
+  if (!side) {
+    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming) != cudaSuccess) {
+      side = nullptr;
+      return s;  // no side stream: the work stays in order on s
+    }
+  }
+  cudaEventRecord(fork_ev, s);
+  cudaStreamWaitEvent(side, fork_ev, 0);
+  return side;
+}
+
+void Workspace::join(cudaStream_t s) {
+  if (!side) return;
+  cudaEventRecord(join_ev, side);
+  cudaStreamWaitEvent(s, join_ev, 0);
+}
+
 float* Workspace::ensure_aux(size_t bytes) {
   if (aux_bytes >= bytes) return aux;
   if (aux) cudaFree(aux);
@@ -470,6 +490,12 @@ int pf_ws_destroy(pf_ws* ws) {
   }
   if (ws->ev0) cudaEventDestroy(ws->ev0);
   if (ws->ev1) cudaEventDestroy(ws->ev1);
+  if (ws->side) {
+    cudaStreamSynchronize(ws->side);
+    cudaStreamDestroy(ws->side);
+    cudaEventDestroy(ws->fork_ev);
+    cudaEventDestroy(ws->join_ev);
+  }
   if (ws->stream) cudaStreamDestroy(ws->stream);
   delete ws;
   return PF_OK;

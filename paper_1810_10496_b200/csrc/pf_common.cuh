@@ -116,6 +116,14 @@ struct Workspace {
   float* aux;
   size_t aux_bytes;
   float* ensure_aux(size_t bytes);  // defined in abi.cu
+  // a side stream for independent work inside one run (abi.cu): fork(s)
+  // returns it ordered after everything enqueued on s so far; join(s) makes
+  // s wait for everything enqueued on the side stream.  Event-timed runs on
+  // s therefore include the side work.
+  cudaStream_t side;
+  cudaEvent_t fork_ev, join_ev;
+  cudaStream_t fork(cudaStream_t s);
+  void join(cudaStream_t s);
 };
 constexpr int kTileFlags = 4096;
 constexpr int kTileFlagsGemm = kTileFlags;  // split-K tile flags

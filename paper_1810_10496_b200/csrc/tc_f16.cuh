@@ -478,15 +478,21 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
   if (strips) {
     // two launches: the strips' shared memory would hold the K-major CTAs to
     // one per SM (2MM 2048: 21 us for one shared launch)
+    // The two launches are independent: the K-major rows go on the
+    // workspace's side stream and overlap the strips (joined before the GEMM).
     f16op::Ops km = ops, mn = ops;
     km.n = mn.n = 0;
     for (int i = 0; i < ops.n; ++i) (ops.op[i].mn ? mn.op[mn.n++] : km.op[km.n++]) = ops.op[i];
     mn.pre_n4 = 0;
-    if (km.n || pre) f16op::f16_split<Bn, V, false><<<dim3(kgrid, km.n + pre), 256, 0, s>>>(km);
     const size_t smem = f16op::strip_smem_bytes(a.K);
     set_smem_attr((const void*)f16op::f16_split<Bn, V, false>, (int)smem);
+    if (km.n || pre) {
+      cudaStream_t ss = ws.fork(s);
+      f16op::f16_split<Bn, V, false><<<dim3(kgrid, km.n + pre), 256, 0, ss>>>(km);
+    }
     f16op::f16_split<Bn, V, false><<<dim3(std::min((rows + f16op::kStrip - 1) / f16op::kStrip, 8 * device_sms()), mn.n),
                                      256, smem, s>>>(mn);
+    if (km.n || pre) ws.join(s);
     return true;
   }
   // K-major rows and (for long K) the column-max pass in one launch, then the transposed tiles
