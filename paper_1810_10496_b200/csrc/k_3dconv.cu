@@ -422,6 +422,9 @@ struct Run {
     } else if ((int64_t)nj * nk >= (int64_t(1) << 31)) {  // int32 plane offsets in the direct form
       launch_s2<V>(A, B, ni, nj, nk, s);
     } else {
+      // Direct-form shapes measured in round 2 (256^3 / 512^3, default 30.7 / 202.8 us):
+      // TY=4 47.1 / 303.1, CH=16 32.8 / 198.7, CH=4 TY=4 49.1 / 337.9, TX=32 TY=4 30.7 / 200.7,
+      // CH=6 30.7 / 206.9 -- none better at the config size.
       switch (c3_mode()) {
         case -1: launch_s2<V>(A, B, ni, nj, nk, s); break;
         default: launch_s2d<V, 2, 2, 8, 64, 2, 1>(A, B, ni, nj, nk, s); break;
