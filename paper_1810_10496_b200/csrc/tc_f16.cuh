@@ -12,7 +12,7 @@
 // the next 11 bits, so hi + lo = x s to 2^-22 relative -- the same 22
 // operand bits as 3xTF32 (whose lo is truncated to TF32 by the tensor core).
 // Elements below 2^-17 of their row's max lose low bits of lo to fp16
-// subnormals; their absolute error stays below 2^-40 of the row max.  The
+// subnormals; their absolute error stays below 2^-39 of the row max.  The
 // product accumulates lo*hi + hi*lo + hi*hi in the fp32 TMEM accumulator and
 // the epilogue multiplies by alpha / (s_row s_col), exactly (powers of two).
 // Per-row scales need no global reduction: a K-major row is scaled by the

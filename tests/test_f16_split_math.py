@@ -5,7 +5,7 @@ Per operand row: s = 2^(15 - e) with max|x| = f 2^e, f in [0.5, 1);
 hi = fp16_rn(x s), lo = fp16_rn(x s - hi).  Claims:
   * x s is exact and max|x s| lies in [2^14, 2^15) (no fp16 overflow);
   * |x s - (hi + lo)| <= 2^-22 |x s| for |x| >= 2^-17 max|x|;
-  * below that, the absolute error stays under 2^-40 max|x| (in x units);
+  * below that, the absolute error stays under 2^-39 max|x| (in x units);
   * a product accumulated as lo*hi + hi*lo + hi*hi matches the fp64 product
     to well inside the 1e-4 tolerance, including rows spanning many decades.
 """
@@ -53,10 +53,10 @@ def test_split_error_bounds():
     rowmax = np.abs(x).max(axis=1, keepdims=True).astype(np.float64)
     big = np.abs(x) >= 2.0**-17 * rowmax
     assert np.all(err[big] <= 2.0**-22 * np.abs(y.astype(np.float64))[big])
-    # in x units: the small elements (lo in fp16 subnormals) below 2^-40 of the row max,
+    # in x units: the small elements (lo in fp16 subnormals) below 2^-39 of the row max,
     # every element below 2^-22 of it
     err_x = err / s.astype(np.float64)
-    assert np.all(err_x[~big] <= (2.0**-40 * rowmax * np.ones_like(err_x))[~big])
+    assert np.all(err_x[~big] <= (2.0**-39 * rowmax * np.ones_like(err_x))[~big])
     assert np.all(err_x <= 2.0**-22 * rowmax)
 
 
