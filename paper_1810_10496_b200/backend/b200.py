@@ -630,18 +630,28 @@ class B200Backend(Backend):
                 # the uploaded arrays ARE this descriptor's input (the runner's
                 # data file); a later generate() for it is a no-op
                 ws.input_tag = (True, int(self.seed), -1)
-            for kernel, orders in jobs:
-                total += self._submit_job(kernel, orders)
+            # the jobs' streams are walked round-robin, chunk by chunk, so the
+            # device has every kernel's first candidates early instead of
+            # idling while the host draws one kernel's whole stream
+            walkers = [self._submit_job(kernel, orders) for kernel, orders in jobs]
+            while walkers:
+                for w in list(walkers):
+                    n = next(w, None)
+                    if n is None:
+                        walkers.remove(w)
+                    else:
+                        total += n
         except _abi.PfError as exc:
             return self._batch_failed(exc) or total
         return total
 
-    def _submit_job(self, kernel: KernelCase, orders) -> int:
+    def _submit_job(self, kernel: KernelCase, orders):
         """Walk ``orders`` (any iterable, e.g. a lazy draw) in geometrically
         growing chunks and submit each chunk's new fresh candidates as one
         batch: the device starts on the first candidates while the host is
-        still compiling the rest of the stream."""
-        seen, total, chunk, pending = set(), 0, 16, []
+        still compiling the rest of the stream.  A generator: yields the
+        number of candidates submitted after each chunk."""
+        seen, chunk, pending = set(), 16, []
         for i, order in enumerate(orders):
             c = self.compile(kernel, order)
             if c.is_ok and c.artifact.digest not in seen:
@@ -649,13 +659,10 @@ class B200Backend(Backend):
                 bench, variant = self.variant_for(kernel, order)
                 pending.append((bench, variant, c.artifact.digest))
             if i + 1 == chunk:
-                if pending:
-                    total += self._submit_cands(kernel, pending)
-                    pending = []
+                yield self._submit_cands(kernel, pending) if pending else 0
+                pending = []
                 chunk *= 4
-        if pending:
-            total += self._submit_cands(kernel, pending)
-        return total
+        yield self._submit_cands(kernel, pending) if pending else 0
 
     def _submit_cands(self, kernel: KernelCase, cands) -> int:
         _, vdims = registry.parse_descriptor(kernel.validation_input)
