@@ -1,5 +1,10 @@
-// Stage-2 contraction kernels, TMA generation: tcgen05 / TMEM 3xTF32 GEMM fed
-// directly from the raw fp32 operands.
+// Stage-2 contraction kernels, TMA generation: tcgen05 / TMEM GEMM in two
+// arithmetic modes -- 3xTF32 fed directly from the raw fp32 operands
+// (kind::tf32), or 3xFP16 fed from row-scaled fp16 hi / lo images
+// (kind::f16, tc_f16.cuh; TmaParams::f16).  A 128-row x 128-byte operand tile
+// is byte-identical in both (32 fp32 or 64 fp16 of K), so the descriptors,
+// ring and warp roles below are shared; the epilogue undoes the 3xFP16 row
+// and column scales.
 //
 //   D = alpha * op(A) op(B) + beta * Cin        (same contract as tc_gemm.cuh)
 //
@@ -29,8 +34,9 @@
 // tc_tma_kernel: one CTA per 128x128 tile (cta_group::1); tc_tma2_kernel: a
 // CTA pair per 256x256 tile (cta_group::2, each CTA streams half of B).
 // Split-K: beta pre-pass + TMA add-reductions (the GEMM launched as a
-// programmatic dependent launch) or, for beta = 0, an in-kernel ordered
-// hand-over through per-tile flags.
+// programmatic dependent launch), or for beta = 0 an in-kernel ordered
+// hand-over through per-tile flags, or -- when the caller already wrote D's
+// base (TcGemmArgs::d_base: zeros or beta * Cin) -- add-reductions only.
 #pragma once
 #include "pf_common.cuh"
 #include "tc_gemm.cuh"
