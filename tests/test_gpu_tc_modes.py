@@ -5,9 +5,9 @@
   is exercised here with inputs spanning many decades and both signs (the
   PolyBench inputs are all O(1)), against an fp64 numpy product, at sizes
   where the f16 path is taken (SYRK from n = 256; plain products from ~1.6k).
-* 3xTF32 (PF_TC_F16=0) and the two-launch CORR/COVAR statistics
-  (PF_CC_FUSED=0) stay available for A/B runs: the tensor-core parity tests
-  are re-run in a subprocess with both switches off.
+* 3xTF32 (PF_TC_F16=0, with CORR/COVAR's two-launch fp32 statistics) stays
+  available for A/B runs: the tensor-core parity tests are re-run in a
+  subprocess with it selected.
 
 Tolerance as everywhere: |t - r| <= max(1e-4 max|r|, 1e-4 |r|).
 """
@@ -103,7 +103,7 @@ def test_syr2k_wide_range():
 
 
 def test_tf32_mode_and_unfused_statistics_still_match():
-    env = dict(os.environ, PF_TC_F16="0", PF_CC_FUSED="0")
+    env = dict(os.environ, PF_TC_F16="0")
     env.pop("PF_PARITY_LOG", None)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         "tests/test_gpu_parity.py", "-k", "tensor_core"],

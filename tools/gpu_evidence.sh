@@ -1,4 +1,4 @@
-# Round-2 final evidence (one GPU): full GPU suite + parity log, smoke, bench
+# Evidence pass (one GPU): full GPU suite + parity log, smoke, bench
 # arms, all-variant report, ncu of the final dense kernels, dense A/B + launch lists.
 O=gpurun_out/ev4
 mkdir -p $O/prof
