@@ -325,6 +325,8 @@ def run_gpu(args, dist: Dist) -> int:
     local_s = sum(step_ms) / 1e3
     max_s = dist.max(local_s)
     value = dist.sum(n_fresh) / max_s
+    # every collective runs on every rank, before the rank-0-only JSON line
+    all_records, all_runs, all_launches = dist.sum(n_records), dist.sum(n_runs), dist.sum(n_launch)
     batch_busy = (be.batch_ms - batch0) / 1e3 / local_s
 
     # ---- end to end: inputs uploaded from pinned host memory every step
@@ -406,8 +408,8 @@ def run_gpu(args, dist: Dist) -> int:
                              "read) before every timed run",
                        "parallelism": f"candidate streams x{dist.world} (one process per GPU, independent)"},
             "fresh_evaluations_per_step": n_fresh / args.steps,
-            "candidate_records_per_s": dist.sum(n_records) / max_s,
-            "device_runs_per_s": dist.sum(n_runs) / max_s,
+            "candidate_records_per_s": all_records / max_s,
+            "device_runs_per_s": all_runs / max_s,
             "valid_fraction": valid / max(1, n_fresh),
             "device_busy_fraction": batch_busy,
             "geomean_speedup": geo,
@@ -416,7 +418,7 @@ def run_gpu(args, dist: Dist) -> int:
             "e2e": e2e,
             "sweep": sweep,
             "cpu_baseline": cpu,
-            "gpu_launches": n_launch,
+            "gpu_launches": int(all_launches),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

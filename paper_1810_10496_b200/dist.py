@@ -21,6 +21,12 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # test hooks: PF_DIST_ONE_DEVICE=1 puts every rank on device 0 and
+        # PF_DIST_BACKEND=gloo forces the gloo control plane (NCCL refuses two
+        # ranks on one GPU) -- the multi-rank paths then run on a one-GPU box
+        if os.environ.get("PF_DIST_ONE_DEVICE") == "1":
+            self.local = 0
+        backend = backend or os.environ.get("PF_DIST_BACKEND") or None
         self.pg = None
         self.device = None
         if self.world > 1:
