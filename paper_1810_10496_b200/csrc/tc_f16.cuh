@@ -54,7 +54,7 @@ struct Ops {
   int n;
   int kp;
   int strips;  // MN-major operands as shared-memory strips (else column maxima + transposed tiles)
-  // optional beta pre-pass riding along in the blockIdx.y == n slice: D = beta * Cin
+  // optional beta pre-pass riding along in the blockIdx.y == n slice: D = beta * Cin (zeros without Cin)
   float4* pre_d;
   const float4* pre_c;
   int64_t pre_n4;
@@ -293,14 +293,14 @@ __global__ void __launch_bounds__(256) f16_split(const Ops ops) {
     for (; i + 3 * stride < ops.pre_n4; i += 4 * stride) {
       float4 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(ops.pre_c + i + u * stride);
+      for (int u = 0; u < 4; ++u) v[u] = ops.pre_c ? __ldg(ops.pre_c + i + u * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         ops.pre_d[i + u * stride] = make_float4(ops.pre_beta * v[u].x, ops.pre_beta * v[u].y,
                                                 ops.pre_beta * v[u].z, ops.pre_beta * v[u].w);
     }
     for (; i < ops.pre_n4; i += stride) {
-      const float4 v = __ldg(ops.pre_c + i);
+      const float4 v = ops.pre_c ? __ldg(ops.pre_c + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       ops.pre_d[i] = make_float4(ops.pre_beta * v.x, ops.pre_beta * v.y, ops.pre_beta * v.z, ops.pre_beta * v.w);
     }
     return;
@@ -467,7 +467,7 @@ inline bool prepare_f16(Workspace& ws, const TcGemmArgs& a, F16Operands& out, cu
   const int pre = base_d ? 1 : 0;
   if (base_d) {
     ops.pre_d = reinterpret_cast<float4*>(a.D);
-    ops.pre_c = reinterpret_cast<const float4*>(a.Cin);
+    ops.pre_c = a.beta != 0.f ? reinterpret_cast<const float4*>(a.Cin) : nullptr;  // beta = 0: zeros
     ops.pre_n4 = (int64_t)a.M * a.N / 4;
     ops.pre_beta = a.beta;
   }

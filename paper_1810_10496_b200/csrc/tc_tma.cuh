@@ -77,6 +77,7 @@ struct TmaParams {
   int upper_only;
   uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides / k-step advance (bytes)
   int idesc_override;                 // probe only: -1 auto, else (a_major | b_major << 1)
+  int sk_tiles, sk_pairs, sk_tiles_n;  // stream-K pair kernel (tc_sk2.cuh): pair tiles, pairs, tiles along N
   int f16;                            // operands are 3xFP16 images (hi/lo fp16, K-major): kind::f16 MMAs
   const float* f16_rinv;              // f16: 1 / row scale per output row (power of two)
   const float* f16_cinv;              // f16: 1 / row scale of op(B)^T per output column
@@ -788,6 +789,7 @@ inline TmaProbe& tma_probe() {
 
 #include "tc_splitk.cuh"  // small products: split-K in a cluster (needs the map helpers above)
 #include "tc_f16.cuh"     // 3xFP16 operand images
+#include "tc_sk2.cuh"     // stream-K pair kernel for plain 3xFP16 products
 
 namespace pf {
 
@@ -820,6 +822,28 @@ inline int tc_tma_splits(int64_t m, int64_t n, int kblocks, bool pair, bool uppe
   splits = std::min(splits, cap);
   const int per = (kblocks + splits - 1) / splits;
   return (kblocks + per - 1) / per;
+}
+
+// Stream-K for plain 3xFP16 products (beta = 0, not symmetric, no split-K)
+// whose pair tiles do not divide evenly over the SM pairs.  PF_TC_SK2=0
+// keeps one tile per pair.
+inline bool tc_sk2_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_TC_SK2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline bool tc_sk2_wanted(int64_t m, int64_t n, int64_t k, bool dual, bool upper, bool sym, float beta) {
+  if (!tc_sk2_enabled() || dual || upper || sym || beta != 0.f || m < 256 || n < 256) return false;
+  const int64_t kb = (k + 63) / 64, tiles = ((m + 255) / 256) * ((n + 255) / 256);
+  const int64_t pairs = std::max(1, device_sms() / 2);
+  if (kb < 8) return false;
+  // several waves with a partial last one (4096^2: 256 tiles on 74 pairs, 3.46
+  // waves: 765 -> 710 us for 2MM).  A single partial wave (2048^2: 64 tiles) is
+  // left alone: the product runs at the power-capped tensor rate there and
+  // spreading it over all 74 pairs measured no faster (46.5 vs 47 us).
+  return tiles > pairs && tiles % pairs != 0;
 }
 
 template <BenchId Bn, int V>
@@ -945,6 +969,17 @@ inline bool launch_tc_tma(const TcGemmArgs& a, cudaStream_t s, bool* dlo_written
   p.D = a.D;
   p.ldd = a.ldd;
   p.upper_only = a.upper_only || p.sym;
+  if (a.f16 && a.d_base && pair && zs == 1 && !p.sym && !a.upper_only && !a.A2 && a.beta == 0.f && p.tma_epi &&
+      tc_sk2_wanted(a.M, a.N, a.K, false, false, false, a.beta)) {
+    const int tn = (int)cdiv(a.N, 256), tiles = tn * (int)cdiv(a.M, 256);
+    p.sk_tiles = tiles;
+    p.sk_tiles_n = tn;
+    p.sk_pairs = (int)std::min<int64_t>(std::max(1, device_sms() / 2), (int64_t)tiles * kblocks);
+    set_smem_attr((const void*)tc_tma2_sk_kernel<Bn, V>, (int)kSk2Smem);
+    tc_tma2_sk_kernel<Bn, V><<<2 * p.sk_pairs, kTmaThreads, kSk2Smem, s>>>(p);
+    if (cudaGetLastError() != cudaSuccess) launch_failed("tcgen05 stream-K contraction launch rejected");
+    return true;
+  }
   set_smem_attr((const void*)tc_tma_kernel<Bn, V>, (int)kTmaSmem);
   set_smem_attr((const void*)tc_tma2_kernel<Bn, V>, (int)kTmaSmem);
   {
@@ -1078,8 +1113,10 @@ inline bool launch_contraction(Workspace& ws, const TcGemmArgs& a0, cudaStream_t
     F16Operands f;
     // symmetric products (beta pre-pass + add-reductions): the pre-pass rides
     // in the operand-split launch when D and Cin are flat, aligned and identical in shape
-    const bool base_d = a.sym && a.Cin && a.ldd == a.N && a.ldc == a.N && a.N % 4 == 0 &&
-                        reinterpret_cast<uintptr_t>(a.D) % 16 == 0 && reinterpret_cast<uintptr_t>(a.Cin) % 16 == 0;
+    const bool flat_d = a.ldd == a.N && a.N % 4 == 0 && reinterpret_cast<uintptr_t>(a.D) % 16 == 0;
+    const bool base_d = (a.sym && a.Cin && flat_d && a.ldc == a.N && reinterpret_cast<uintptr_t>(a.Cin) % 16 == 0) ||
+                        // stream-K adds every partial tile onto D: zeros written by the split launch
+                        (flat_d && tc_sk2_wanted(a.M, a.N, a.K, a.A2 != nullptr, a.upper_only != 0, a.sym != 0, a.beta));
     if (prepare_f16<Bn, V>(ws, a, f, s, base_d)) {
       TcGemmArgs b = a;
       b.f16 = &f;

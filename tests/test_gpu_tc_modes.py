@@ -145,3 +145,17 @@ def test_corrcov_both_statistics_paths(bench, dims):
     assert len(outs) == len(ref)
     for got, r in zip(outs, ref):
         _check(got, np.asarray(r))
+
+
+def test_2mm_stream_k():
+    """Pair tiles over several waves with a partial last one (2304^2: 81 tiles
+    on 74 SM pairs): the stream-K pair kernel (tc_sk2.cuh) splits tiles across
+    pairs and adds the partial tiles onto a zeroed D."""
+    n = 2304
+    rng = np.random.default_rng(13)
+    A = _wide(rng, (n, n), 4)
+    B = _wide(rng, (n, n), 4)
+    D = _wide(rng, (n, n), 2)
+    C, E = (o.reshape(n, n) for o in _run("2MM", (n, n, n, n), {0: A, 1: B, 3: D}, [2, 4]))
+    _check(C, A.astype(np.float64) @ B.astype(np.float64))
+    _check(E, C.astype(np.float64) @ D.astype(np.float64))
