@@ -377,6 +377,24 @@ __device__ __forceinline__ void update2(const float (&q)[64], float (&a)[2][64],
   }
 }
 
+// update2 for one register column (same summation order as update2's
+// column 0): the pivot warp's second column after its first column's pivot,
+// the step on the critical path of the own-panel factorisation.
+__device__ __forceinline__ void update1(const float (&q)[64], float (&a)[64], float* rdst, int lane) {
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 64; i += 4) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[e] = fmaf(q[i + e], a[i + e], s[e]);
+  }
+  float r = (s[0] + s[1]) + (s[2] + s[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  if (lane == 0) *rdst = r;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) a[i] = fmaf(-q[i], r, a[i]);
+}
+
 template <BenchId Bn, int V, int W>
 __global__ void __launch_bounds__(16 * W, 1) gs_panel2(float* __restrict__ A, float* __restrict__ R,
                                                               float* __restrict__ Q, float* __restrict__ qbuf,
@@ -388,6 +406,8 @@ __global__ void __launch_bounds__(16 * W, 1) gs_panel2(float* __restrict__ A, fl
   __shared__ float rbuf[W * W];                  // own panel's R block, written out after the factorisation
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int b = blockIdx.x, c0 = b * W, w = min(W, n - c0);
+  const bool named_bar = (trace & 2) != 0;  // PF_GS_NB=1: the own-panel steps meet at named barriers
+  trace &= 1;
   float* st = qpan;  // staging for the panel load / store: 128 rows x (W + 1)
   if (t < W) {  // ordered before use by the load loop's barriers
     const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&slot_bar[t]));
@@ -539,11 +559,26 @@ __global__ void __launch_bounds__(16 * W, 1) gs_panel2(float* __restrict__ A, fl
         pivot(a[0], rdiag[0]);
       if (trace && b == 5 && lane == 0) gs_trace_step(R, n, kk, 0);
     }
-    const int nthreads = 32 * (last_warp - pw + 1);  // the pivot warp and every warp after it
-    if (consumer)
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + (kk & 1)), "r"(nthreads) : "memory");
-    else
-      asm volatile("bar.arrive %0, %1;" ::"r"(1 + (kk & 1)), "r"(nthreads) : "memory");
+    if (named_bar) {
+      const int nthreads = 32 * (last_warp - pw + 1);  // the pivot warp and every warp after it
+      if (consumer)
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + (kk & 1)), "r"(nthreads) : "memory");
+      else
+        asm volatile("bar.arrive %0, %1;" ::"r"(1 + (kk & 1)), "r"(nthreads) : "memory");
+    } else if (consumer && !producer) {
+      // slots are written once, so a consumer only waits for slot kk's
+      // mbarrier (the pivot's release); no warp waits for a slower consumer
+      const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&slot_bar[kk]));
+      uint32_t ok = 0;
+      do {
+        asm volatile(
+            "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], 0;\n\t"
+            "selp.b32 %0, 1, 0, P;\n\t}"
+            : "=r"(ok)
+            : "r"(bar)
+            : "memory");
+      } while (!ok);
+    }
     if (!consumer) continue;  // (a pure producer has no later column: it leaves at the next check)
     if (trace && b == 5 && warp == last_warp && lane == 0) gs_trace_step(R, n, kk, 1);
     float q[64];
@@ -555,8 +590,11 @@ __global__ void __launch_bounds__(16 * W, 1) gs_panel2(float* __restrict__ A, fl
       q[4 * g + 2] = v.z;
       q[4 * g + 3] = v.w;
     }
-    update2(q, a, 2 * warp < w && 2 * warp > kk, 2 * warp + 1 < w && 2 * warp + 1 > kk, rbuf + kk * W + 2 * warp,
-            lane);
+    if (2 * warp > kk || named_bar)
+      update2(q, a, 2 * warp < w && 2 * warp > kk, 2 * warp + 1 < w && 2 * warp + 1 > kk, rbuf + kk * W + 2 * warp,
+              lane);
+    else  // the warp's first column is factored; its second (a consumer's last column > kk) pivots next
+      update1(q, a[1], rbuf + kk * W + 2 * warp + 1, lane);
     if (trace && b == 5 && warp == last_warp && lane == 0) gs_trace_step(R, n, kk, 2);
   }
   if (warp == 0) {  // publisher
@@ -664,7 +702,8 @@ void launch_panel2(Workspace& ws, cudaStream_t s) {
   float* Q = ws.a.p[2];
   static const int trace = [] {
     const char* e = std::getenv("PF_GS_TRACE");
-    return e && e[0] == '1' ? 1 : 0;
+    const char* nb = std::getenv("PF_GS_NB");
+    return (e && e[0] == '1' ? 1 : 0) | (nb && nb[0] == '1' ? 2 : 0);
   }();
   static const int width = [] {
     const char* e = std::getenv("PF_GS_W");

@@ -79,7 +79,9 @@ CASES = {
     "SYR2K": [((2048, 2048), ["stage0-reg", "stage1", "stage2"])],
     "CORR": [((2048, 2048), ["baseline", "stage1", "stage2"])],
     "COVAR": [((2048, 2048), ["baseline", "stage1", "stage2"])],
-    "GRAMSCHM": [((2048, 2048), ["baseline", "stage1", "stage2"])],
+    # ragged panels of the persistent stage-2 kernel: last panel partial, m not a multiple of 128
+    "GRAMSCHM": [((2048, 2048), ["baseline", "stage1", "stage2"]), ((1999, 1999), ["stage2"]),
+                 ((2048, 1000), ["stage2"])],
 }
 
 
