@@ -538,9 +538,12 @@ class B200Backend(Backend):
         a single sample (their relative jitter is already far below 1%)."""
         key = (ws.bench, ws.dims, variant)
         if variant not in ws.warm:
-            ws.run(variant, samples=1, batch=1, restore=True, flush=False)
             first = ws.run(variant, samples=1, batch=1, restore=True, flush=False)[0]
-            self._count(ws.bench, variant, ws.dims, 2)
+            warmups = 1
+            if first <= self.slow_ms:  # a slow run's one-time costs are below its jitter: one warm-up
+                first = ws.run(variant, samples=1, batch=1, restore=True, flush=False)[0]
+                warmups = 2
+            self._count(ws.bench, variant, ws.dims, warmups)
             ws.warm.add(variant)
             self._first_ms[key] = first
             if key not in self._batch:
@@ -556,7 +559,7 @@ class B200Backend(Backend):
 
     def prewarm(self, kernel: KernelCase) -> int:
         """Give every variant of ``kernel``'s family its first-use warm-up
-        (module load, scratch, graph capture, batch sizing: the two untimed
+        (module load, scratch, graph capture, batch sizing: the untimed
         runs ``_timed`` / the prefetch do on first use) at the measurement
         size, so later measurements are steady-state.  Returns the number of
         variants warmed."""
@@ -567,9 +570,12 @@ class B200Backend(Backend):
         for v in range(len(family(bench).knobs)):
             if v in ws.warm or not self._supported(bench, v, mdims):
                 continue
-            ws.run(v, samples=1, batch=1, restore=True, flush=False)
             first = ws.run(v, samples=1, batch=1, restore=True, flush=False)[0]
-            self._count(bench, v, mdims, 2)
+            warmups = 1
+            if first <= self.slow_ms:
+                first = ws.run(v, samples=1, batch=1, restore=True, flush=False)[0]
+                warmups = 2
+            self._count(bench, v, mdims, warmups)
             ws.warm.add(v)
             key = (bench, ws.dims, v)
             self._first_ms[key] = first
@@ -604,8 +610,8 @@ class B200Backend(Backend):
         host prepares job k+1 (and the engine walks job k's records) while
         the device runs job k.  Per candidate: one validation run on the
         stock validation input (outputs copied back) and the measurement
-        protocol of ``execute`` (first use: two warm-up runs that size the
-        batch of us-scale kernels; then ``samples`` timed samples, each after
+        protocol of ``execute`` (first use: two warm-up runs -- one for a run
+        slower than ``slow_ms`` -- that size the batch of us-scale kernels; then ``samples`` timed samples, each after
         an L2 flush; median).  ``host_inputs`` maps (kernel id, "validation"
         | "measurement") to {array index: pinned host pointer}: those inputs
         are uploaded first, asynchronously on the copy stream (the end-to-end
@@ -675,13 +681,20 @@ class B200Backend(Backend):
             if variant not in mws.warm and (mws, variant) not in cold:
                 cold.append((mws, variant))
         if cold:
-            ms = self._worker_submit([_eval_item(ws, v) for ws, v in cold for _ in range(2)]).result()
+            # one warm-up each; a second one only for runs not slower than
+            # slow_ms (a slow run's one-time costs are below its jitter)
+            ms = self._worker_submit([_eval_item(ws, v) for ws, v in cold]).result()
+            again = [i for i, t in enumerate(ms) if t <= self.slow_ms]
+            if again:
+                ms2 = self._worker_submit([_eval_item(*cold[i]) for i in again]).result()
+                for i, t in zip(again, ms2):
+                    ms[i] = t
             for i, (ws, variant) in enumerate(cold):
                 key = (ws.bench, ws.dims, variant)
-                first = ms[2 * i + 1]
+                first = ms[i]
                 ws.warm.add(variant)
                 self._first_ms[key] = first
-                self._count(ws.bench, variant, ws.dims, 2)
+                self._count(ws.bench, variant, ws.dims, 2 if i in again else 1)
                 if key not in self._batch:
                     self._batch[key] = (min(self.max_batch, max(1, int(self.min_sample_ms / max(first, 1e-4)) + 1))
                                         if first < self.min_sample_ms else 1)
