@@ -41,6 +41,7 @@ import ctypes
 import gzip
 import json
 import operator
+import os
 import statistics
 import sys
 from collections import OrderedDict
@@ -325,6 +326,8 @@ class B200Backend(Backend):
         self.measurement_cache: dict | None = None
         # pure-function memos: compile is pure in (kernel, order)
         self._variant_memo: dict[tuple, int] = {}
+        self._order_memo: dict[tuple, tuple] = {}  # (id(order), bench) -> (order, variant)
+        self._use_order_memo = os.environ.get("PF_ORDER_MEMO", "1") != "0"
         self._supported_memo: dict[tuple, bool] = {}
         self._compile_memo: dict[tuple, object] = {}
         # results of the last prefetch, consumed by execute():
@@ -347,13 +350,26 @@ class B200Backend(Backend):
 
     def variant_for(self, kernel: KernelCase, order) -> tuple[str, int]:
         bench = registry.bench_of(kernel)
+        # the engine asks about the same order objects several times (the
+        # prefetch walk, explore's compile, the record): an identity memo
+        # skips re-keying up to 256 pass names per call (the order is kept
+        # alive by the memo, so its id cannot be reused while it is there)
+        hit = self._order_memo.get((id(order), bench))
+        if hit is not None and hit[0] is order:
+            return bench, hit[1]
         key = (bench, tuple(map(_NAME, order.passes)))
         v = self._variant_memo.get(key)
         if v is None:
-            if not isinstance(order, PhaseOrder):  # a foreign (reference) PhaseOrder: same pass names
-                order = PhaseOrder(tuple(PassId(p.name) for p in order.passes))
-            v = family(bench).select(passmodel.interpret(order))
+            if isinstance(order, PhaseOrder):
+                own = order
+            else:  # a foreign (reference) PhaseOrder: same pass names
+                own = PhaseOrder(tuple(PassId(p.name) for p in order.passes))
+            v = family(bench).select(passmodel.interpret(own))
             self._variant_memo[key] = v
+        if self._use_order_memo:
+            if len(self._order_memo) >= 1 << 18:
+                self._order_memo.clear()
+            self._order_memo[(id(order), bench)] = (order, v)
         return bench, v
 
     def artifact(self, bench: str, variant: int):
